@@ -1,0 +1,94 @@
+"""ctypes binding of libbp_b200.so (the C ABI declared in include/bp_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2008_04397_b200/csrc``).  There is no fallback: if the
+library is missing or CUDA is unavailable every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbp_b200.so")
+
+OK = 0
+ERR_RUNAWAY = 1
+ERR_MIDPOINT = 2
+ERR_DOMAIN = 3
+EINVAL = -1
+ECUDA = -2
+ARITH_PARITY = 0
+ARITH_FAST = 1
+
+# every symbol include/bp_b200.h declares (checked by tests/test_capi_symbols.py)
+EXPORTS = (
+    "bp_version", "bp_last_error", "bp_fused_span", "bp_push_span",
+    "bp_deposit_span", "bp_gather_span", "bp_fused_span_ex",
+    "bp_fused_span_host", "bp_sort_by_cell", "bp_cell_keys",
+    "bp_fold_periodic_i64",
+)
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_INT = ctypes.c_int
+
+_SIGS = {
+    "bp_version": (_INT, []),
+    "bp_last_error": (ctypes.c_char_p, []),
+    "bp_fused_span": (_INT, [_INT, _INT] + [_P] * 7 + [_I64, _I64] + [_P] * 4
+                      + [_P, _P, _P] + [_D] * 5 + [_INT, _D, _INT, _P, _P]),
+    "bp_fused_span_ex": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]
+                         + [_P] * 4 + [_P, _P, _P] + [_D] * 5
+                         + [_INT, _D, _INT, _P, _P]),
+    "bp_push_span": (_INT, [_INT, _INT] + [_P] * 6 + [_I64, _I64, _P, _P]
+                     + [_P, _P, _P] + [_D] * 5 + [_INT, _INT, _INT, _P, _P]),
+    "bp_deposit_span": (_INT, [_INT, _INT] + [_P] * 7 + [_I64, _I64, _P, _P,
+                                                        _P, _P, _D, _D, _P, _P]),
+    "bp_gather_span": (_INT, [_INT, _INT, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                              _P, _D, _P, _P, _P]),
+    "bp_fused_span_host": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]
+                           + [_P] * 4 + [_P, _P, _P] + [_D] * 5
+                           + [_INT, _D, _INT, _I64]),
+    "bp_sort_by_cell": (_INT, [_INT] + [_P] * 7 + [_P, _I64, _P, _P, _P, _P]),
+    "bp_cell_keys": (_INT, [_INT, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "bp_fold_periodic_i64": (_INT, [_P, _I64, _P, _P]),
+}
+
+_lib = None
+
+
+class BackendError(RuntimeError):
+    """The CUDA library is missing or a call failed at the CUDA level."""
+
+
+def load():
+    """Load libbp_b200.so (no GPU needed to load; calls need one)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BackendError(
+            f"{LIB_PATH} is not built; run __graft_entry__.build() or "
+            f"make -C {os.path.join(_HERE, 'csrc')}")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error():
+    return load().bp_last_error().decode(errors="replace")
+
+
+def check(rc, what):
+    """Raise for negative (call-level) return codes; pass statuses through."""
+    if rc < 0:
+        kind = "invalid argument" if rc == EINVAL else "CUDA failure"
+        raise BackendError(f"{what}: {kind}: {last_error()}")
+    return rc

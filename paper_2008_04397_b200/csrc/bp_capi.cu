@@ -1,0 +1,421 @@
+// C ABI (include/bp_b200.h): argument checking, status handling, and the
+// host-memory streaming pipeline.  Kernels live in bp_parity.cu (bitwise
+// reference arithmetic) and bp_fast.cu (FMA / native f32 arithmetic).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/bp_b200.h"
+#include "bp_launch.h"
+
+namespace bp {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+              const double* origin, const double* spacing, const int64_t* counts,
+              int64_t* keys, cudaStream_t s);
+int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, void* ws,
+                 void* qs, int64_t* ids, int64_t n, const double* origin,
+                 const double* spacing, const int64_t* counts, cudaStream_t s);
+int fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, cudaStream_t s);
+
+namespace {
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return BP_ECUDA;
+  }
+  return BP_OK;
+}
+
+bool valid_pair(int pb, int fb) {
+  return (pb == 8 && fb == 8) || (pb == 4 && fb == 4) || (pb == 4 && fb == 8);
+}
+
+int check_geo(const double* geo_g, const int64_t* geo_i) {
+  if (!geo_g || !geo_i) {
+    set_error("geometry arrays are required");
+    return BP_EINVAL;
+  }
+  for (int a = 0; a < 3; ++a) {
+    if (geo_i[a] < 1) {
+      set_error("cell counts must be >= 1");
+      return BP_EINVAL;
+    }
+    if (geo_i[3 + a] != 0 && geo_i[3 + a] != 1) {
+      set_error("boundary codes must be 0 (periodic) or 1 (reflecting)");
+      return BP_EINVAL;
+    }
+    if (!(geo_g[a] > 0.0)) {
+      set_error("grid spacings must be positive");
+      return BP_EINVAL;
+    }
+  }
+  const int64_t nn = (geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
+  if (nn * 10 >= (int64_t)1 << 31) {
+    set_error("grid of %lld nodes exceeds the 32-bit node index space", (long long)nn);
+    return BP_EINVAL;
+  }
+  return BP_OK;
+}
+
+// Per-thread status slot for the synchronous (d_status == NULL) form.
+struct StatusSlot {
+  int* d = nullptr;
+  int* h = nullptr;
+  int dev = -1;
+};
+static thread_local StatusSlot g_slot;
+
+int* sync_slot(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_slot.d == nullptr || g_slot.dev != dev) {
+    if (cudaMalloc((void**)&g_slot.d, sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMallocHost((void**)&g_slot.h, sizeof(int)) != cudaSuccess) return nullptr;
+    g_slot.dev = dev;
+  }
+  cudaMemsetAsync(g_slot.d, 0, sizeof(int), s);
+  return g_slot.d;
+}
+
+int finish(int rc, bool sync, cudaStream_t s) {
+  if (rc != BP_OK || !sync) return rc;
+  rc = cuda_check(cudaMemcpyAsync(g_slot.h, g_slot.d, sizeof(int), cudaMemcpyDeviceToHost, s),
+                  "status copy");
+  if (rc) return rc;
+  rc = cuda_check(cudaStreamSynchronize(s), "kernel execution");
+  if (rc) return rc;
+  return *g_slot.h;
+}
+
+int run(Call& c, int arith, int* d_status, cudaStream_t s) {
+  if (c.count < 0 || c.start < 0) {
+    set_error("negative span (%lld, %lld)", (long long)c.start, (long long)c.count);
+    return BP_EINVAL;
+  }
+  const bool sync = d_status == nullptr;
+  if (c.count == 0) return BP_OK;
+  c.status = sync ? sync_slot(s) : d_status;
+  if (!c.status) {
+    set_error("status slot allocation failed");
+    return BP_ECUDA;
+  }
+  int rc;
+  if (arith == BP_ARITH_PARITY) rc = launch_parity(c, s);
+  else if (arith == BP_ARITH_FAST) rc = launch_fast(c, s);
+  else {
+    set_error("unknown arithmetic mode %d", arith);
+    rc = BP_EINVAL;
+  }
+  return finish(rc, sync, s);
+}
+
+void fill_geo(Call& c, const double* geo_f, const double* geo_g, const int64_t* geo_i) {
+  for (int k = 0; k < 9; ++k) {
+    c.geo_f[k] = geo_f ? geo_f[k] : 0.0;
+    c.geo_g[k] = geo_g[k];
+  }
+  for (int k = 0; k < 6; ++k) c.geo_i[k] = geo_i[k];
+}
+
+int fused_call(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
+               void* vs, void* ws, const void* qs, int64_t start, int64_t count, const void* E,
+               const void* B, int64_t* acc, const void* invvol, const double* geo_f,
+               const double* geo_g, const int64_t* geo_i, double dt, double dth, double qdt2m,
+               double beta, double one, int n_iters, double scale, int mixed, int* d_status,
+               cudaStream_t s) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  if (!geo_f || n_iters < 0) {
+    set_error("geo_f required and n_iters >= 0");
+    return BP_EINVAL;
+  }
+  Call c{};
+  c.op = OP_FUSED;
+  c.pbytes = pbytes; c.fbytes = fbytes;
+  c.x = xs; c.y = ys; c.z = zs; c.u = us; c.v = vs; c.w = ws; c.q = qs;
+  c.start = start; c.count = count;
+  c.E = E; c.B = B; c.acc = acc; c.invvol = invvol;
+  fill_geo(c, geo_f, geo_g, geo_i);
+  c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
+  c.n_iters = n_iters; c.mixed = mixed; c.apply_bc = 1;
+  return run(c, arith, d_status, s);
+}
+
+// ---------------------------------------------------------------------------
+// Host-memory streaming pipeline (bp_fused_span_host).
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ready[2];
+  void* slot[2][7] = {};
+  size_t slot_bytes = 0;
+  void* dE = nullptr;
+  void* dB = nullptr;
+  void* dinv = nullptr;
+  int64_t* dacc = nullptr;
+  size_t field_bytes = 0, acc_bytes = 0;
+  int* dstatus = nullptr;
+  int* hstatus = nullptr;
+};
+static std::mutex g_host_mu;
+static HostCtx g_host;
+
+int host_ctx_reserve(HostCtx& h, size_t slot_bytes, size_t field_bytes, size_t acc_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (h.dev != dev) {
+    h = HostCtx();
+    h.dev = dev;
+    for (int k = 0; k < 2; ++k) {
+      if (cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h.ready[k], cudaEventDisableTiming) != cudaSuccess)
+        return cuda_check(cudaGetLastError(), "stream create");
+    }
+    if (cudaMalloc((void**)&h.dstatus, sizeof(int)) != cudaSuccess ||
+        cudaMallocHost((void**)&h.hstatus, sizeof(int)) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "status alloc");
+  }
+  if (slot_bytes > h.slot_bytes) {
+    for (int k = 0; k < 2; ++k)
+      for (int a = 0; a < 7; ++a) {
+        if (h.slot[k][a]) cudaFree(h.slot[k][a]);
+        if (cudaMalloc(&h.slot[k][a], slot_bytes) != cudaSuccess)
+          return cuda_check(cudaGetLastError(), "slot alloc");
+      }
+    h.slot_bytes = slot_bytes;
+  }
+  if (field_bytes > h.field_bytes) {
+    if (h.dE) { cudaFree(h.dE); cudaFree(h.dB); cudaFree(h.dinv); }
+    if (cudaMalloc(&h.dE, field_bytes) != cudaSuccess || cudaMalloc(&h.dB, field_bytes) != cudaSuccess ||
+        cudaMalloc(&h.dinv, field_bytes / 3 + 64) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "field alloc");
+    h.field_bytes = field_bytes;
+  }
+  if (acc_bytes > h.acc_bytes) {
+    if (h.dacc) cudaFree(h.dacc);
+    if (cudaMalloc((void**)&h.dacc, acc_bytes) != cudaSuccess)
+      return cuda_check(cudaGetLastError(), "acc alloc");
+    h.acc_bytes = acc_bytes;
+  }
+  return BP_OK;
+}
+
+}  // namespace
+}  // namespace bp
+
+using namespace bp;
+
+extern "C" {
+
+int bp_version(void) { return 100; }
+
+const char* bp_last_error(void) { return g_err; }
+
+int bp_fused_span(int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us, void* vs,
+                  void* ws, const void* qs, int64_t start, int64_t count, const void* E,
+                  const void* B, int64_t* acc, const void* invvol, const double* geo_f,
+                  const double* geo_g, const int64_t* geo_i, double dt, double dth,
+                  double qdt2m, double beta, double one, int n_iters, double scale, int mixed,
+                  int* d_status, void* stream) {
+  return fused_call(BP_ARITH_PARITY, pbytes, fbytes, xs, ys, zs, us, vs, ws, qs, start, count,
+                    E, B, acc, invvol, geo_f, geo_g, geo_i, dt, dth, qdt2m, beta, one, n_iters,
+                    scale, mixed, d_status, (cudaStream_t)stream);
+}
+
+int bp_fused_span_ex(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
+                     void* vs, void* ws, const void* qs, int64_t start, int64_t count,
+                     const void* E, const void* B, int64_t* acc, const void* invvol,
+                     const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
+                     double dth, double qdt2m, double beta, double one, int n_iters,
+                     double scale, int mixed, int* d_status, void* stream) {
+  return fused_call(arith, pbytes, fbytes, xs, ys, zs, us, vs, ws, qs, start, count, E, B, acc,
+                    invvol, geo_f, geo_g, geo_i, dt, dth, qdt2m, beta, one, n_iters, scale,
+                    mixed, d_status, (cudaStream_t)stream);
+}
+
+int bp_push_span(int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us, void* vs,
+                 void* ws, int64_t start, int64_t count, const void* E, const void* B,
+                 const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
+                 double dth, double qdt2m, double beta, double one, int n_iters, int apply_bc,
+                 int mixed, int* d_status, void* stream) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  if (!geo_f) {
+    set_error("geo_f required");
+    return BP_EINVAL;
+  }
+  Call c{};
+  c.op = OP_PUSH;
+  c.pbytes = pbytes; c.fbytes = fbytes;
+  c.x = xs; c.y = ys; c.z = zs; c.u = us; c.v = vs; c.w = ws;
+  c.start = start; c.count = count;
+  c.E = E; c.B = B;
+  fill_geo(c, geo_f, geo_g, geo_i);
+  c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one;
+  c.n_iters = n_iters; c.mixed = mixed; c.apply_bc = apply_bc ? 1 : 0;
+  return run(c, BP_ARITH_PARITY, d_status, (cudaStream_t)stream);
+}
+
+int bp_deposit_span(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs,
+                    const void* us, const void* vs, const void* ws, const void* qs,
+                    int64_t start, int64_t count, int64_t* acc, const void* invvol,
+                    const double* geo_g, const int64_t* geo_i, double one, double scale,
+                    int* d_status, void* stream) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  Call c{};
+  c.op = OP_DEPOSIT;
+  c.pbytes = pbytes; c.fbytes = fbytes;
+  c.x = (void*)xs; c.y = (void*)ys; c.z = (void*)zs;
+  c.u = (void*)us; c.v = (void*)vs; c.w = (void*)ws; c.q = qs;
+  c.start = start; c.count = count;
+  c.acc = acc; c.invvol = invvol;
+  fill_geo(c, nullptr, geo_g, geo_i);
+  c.one = one; c.scale = scale;
+  return run(c, BP_ARITH_PARITY, d_status, (cudaStream_t)stream);
+}
+
+int bp_gather_span(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs,
+                   int64_t start, int64_t count, const void* E, const void* B,
+                   const double* geo_g, const int64_t* geo_i, double one, void* out,
+                   int* d_status, void* stream) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  Call c{};
+  c.op = OP_GATHER;
+  c.pbytes = pbytes; c.fbytes = fbytes;
+  c.x = (void*)xs; c.y = (void*)ys; c.z = (void*)zs;
+  c.start = start; c.count = count;
+  c.E = E; c.B = B; c.out = out;
+  fill_geo(c, nullptr, geo_g, geo_i);
+  c.one = one;
+  return run(c, BP_ARITH_PARITY, d_status, (cudaStream_t)stream);
+}
+
+int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs,
+                       void* us, void* vs, void* ws, const void* qs, int64_t start,
+                       int64_t count, const void* E, const void* B, int64_t* acc,
+                       const void* invvol, const double* geo_f, const double* geo_g,
+                       const int64_t* geo_i, double dt, double dth, double qdt2m, double beta,
+                       double one, int n_iters, double scale, int mixed,
+                       int64_t batch_particles) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  if (count < 0 || start < 0) {
+    set_error("negative span");
+    return BP_EINVAL;
+  }
+  if (count == 0) return BP_OK;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  HostCtx& h = g_host;
+  const int64_t nn = (geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
+  int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 23);
+  if (batch > count) batch = count;
+  rc = host_ctx_reserve(h, (size_t)batch * pbytes, (size_t)3 * nn * fbytes,
+                        (size_t)10 * nn * sizeof(int64_t));
+  if (rc) return rc;
+  cudaStream_t s0 = h.st[0];
+  // fields, invvol and the caller's accumulator go up once
+  rc |= cuda_check(cudaMemcpyAsync(h.dE, E, 3 * nn * fbytes, cudaMemcpyHostToDevice, s0), "E h2d");
+  rc |= cuda_check(cudaMemcpyAsync(h.dB, B, 3 * nn * fbytes, cudaMemcpyHostToDevice, s0), "B h2d");
+  rc |= cuda_check(cudaMemcpyAsync(h.dinv, invvol, nn * fbytes, cudaMemcpyHostToDevice, s0), "invvol h2d");
+  rc |= cuda_check(cudaMemcpyAsync(h.dacc, acc, 10 * nn * 8, cudaMemcpyHostToDevice, s0), "acc h2d");
+  rc |= cuda_check(cudaMemsetAsync(h.dstatus, 0, sizeof(int), s0), "status");
+  rc |= cuda_check(cudaEventRecord(h.ready[0], s0), "event");
+  if (rc) return BP_ECUDA;
+  rc |= cuda_check(cudaStreamWaitEvent(h.st[1], h.ready[0], 0), "wait");
+  char* host[7] = {(char*)xs, (char*)ys, (char*)zs, (char*)us, (char*)vs, (char*)ws, (char*)qs};
+  int64_t b = 0;
+  for (int64_t off = 0; off < count && !rc; off += batch, ++b) {
+    const int k = (int)(b & 1);
+    cudaStream_t s = h.st[k];
+    const int64_t n = (count - off < batch) ? count - off : batch;
+    const size_t bytes = (size_t)n * pbytes;
+    const size_t hoff = (size_t)(start + off) * pbytes;
+    for (int a = 0; a < 7 && !rc; ++a)
+      rc = cuda_check(cudaMemcpyAsync(h.slot[k][a], host[a] + hoff, bytes,
+                                      cudaMemcpyHostToDevice, s), "batch h2d");
+    if (rc) break;
+    Call c{};
+    c.op = OP_FUSED;
+    c.pbytes = pbytes; c.fbytes = fbytes;
+    c.x = h.slot[k][0]; c.y = h.slot[k][1]; c.z = h.slot[k][2];
+    c.u = h.slot[k][3]; c.v = h.slot[k][4]; c.w = h.slot[k][5]; c.q = h.slot[k][6];
+    c.start = 0; c.count = n;
+    c.E = h.dE; c.B = h.dB; c.acc = h.dacc; c.invvol = h.dinv;
+    fill_geo(c, geo_f, geo_g, geo_i);
+    c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
+    c.n_iters = n_iters; c.mixed = mixed; c.apply_bc = 1;
+    c.status = h.dstatus;
+    rc = arith == BP_ARITH_FAST ? launch_fast(c, s) : launch_parity(c, s);
+    if (rc) break;
+    for (int a = 0; a < 6 && !rc; ++a)
+      rc = cuda_check(cudaMemcpyAsync(host[a] + hoff, h.slot[k][a], bytes,
+                                      cudaMemcpyDeviceToHost, s), "batch d2h");
+  }
+  // join both streams, bring the accumulator and status back
+  cudaEventRecord(h.ready[1], h.st[1]);
+  cudaStreamWaitEvent(s0, h.ready[1], 0);
+  if (!rc) rc = cuda_check(cudaMemcpyAsync(acc, h.dacc, 10 * nn * 8, cudaMemcpyDeviceToHost, s0), "acc d2h");
+  if (!rc) rc = cuda_check(cudaMemcpyAsync(h.hstatus, h.dstatus, sizeof(int), cudaMemcpyDeviceToHost, s0), "status d2h");
+  int rc2 = cuda_check(cudaStreamSynchronize(s0), "pipeline");
+  if (rc) return rc;
+  if (rc2) return rc2;
+  return *h.hstatus;
+}
+
+int bp_sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, void* ws,
+                    void* qs, int64_t* ids, int64_t n, const double* origin,
+                    const double* spacing, const int64_t* counts, void* stream) {
+  if (pbytes != 4 && pbytes != 8) {
+    set_error("unsupported particle dtype (%d bytes)", pbytes);
+    return BP_EINVAL;
+  }
+  return sort_by_cell(pbytes, xs, ys, zs, us, vs, ws, qs, ids, n, origin, spacing, counts,
+                      (cudaStream_t)stream);
+}
+
+int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+                 const double* origin, const double* spacing, const int64_t* counts,
+                 int64_t* keys, void* stream) {
+  return cell_keys(pbytes, xs, ys, zs, n, origin, spacing, counts, keys, (cudaStream_t)stream);
+}
+
+int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void* stream) {
+  return fold_periodic_i64(acc, rows, geo_i, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,36 @@
+// Internal interface between the C ABI (bp_capi.cu) and the kernel
+// translation units (bp_parity.cu: -fmad=false, bp_fast.cu: FMA).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bp {
+
+enum Op { OP_FUSED = 0, OP_PUSH = 1, OP_DEPOSIT = 2, OP_GATHER = 3 };
+
+// One span call, reference argument meaning (kernels.py:82,310,385,458).
+struct Call {
+  int op;
+  int pbytes, fbytes;
+  void *x, *y, *z, *u, *v, *w;
+  const void* q;
+  int64_t start, count;
+  const void* E;
+  const void* B;
+  int64_t* acc;
+  const void* invvol;
+  double geo_f[9], geo_g[9];
+  int64_t geo_i[6];
+  double dt, dth, qdt2m, beta, one, scale;
+  int n_iters, mixed, apply_bc;
+  void* out;    // gather rows
+  int* status;  // device int, atomicMax
+};
+
+// Return 0 on a successful enqueue, else a negative BP_E* code.
+int launch_parity(const Call& c, cudaStream_t s);
+int launch_fast(const Call& c, cudaStream_t s);
+
+void set_error(const char* fmt, ...);
+
+}  // namespace bp

@@ -1,0 +1,119 @@
+// Parity build of the span kernels: compiled with -fmad=false and IEEE
+// division so every particle follows the reference numba arithmetic bit for
+// bit (kernels.py:458-735).
+#include <cstdio>
+
+#include "bp_launch.h"
+#include "bp_span.cuh"
+
+namespace bp {
+
+namespace {
+
+template <typename P, typename F>
+SpanParams<P, F> make_params(const Call& c) {
+  SpanParams<P, F> a;
+  a.x = (P*)c.x; a.y = (P*)c.y; a.z = (P*)c.z;
+  a.u = (P*)c.u; a.v = (P*)c.v; a.w = (P*)c.w;
+  a.q = (const P*)c.q;
+  a.start = c.start; a.count = c.count;
+  a.E = (const F*)c.E; a.B = (const F*)c.B;
+  a.acc = (i64*)c.acc;
+  a.invvol = (const F*)c.invvol;
+  a.ox = (P)c.geo_f[3]; a.oy = (P)c.geo_f[4]; a.oz = (P)c.geo_f[5];
+  a.Lx = (P)c.geo_f[6]; a.Ly = (P)c.geo_f[7]; a.Lz = (P)c.geo_f[8];
+  // ox + Lx and (ox+Lx) + (ox+Lx) in particle precision (kernels.py:507-533)
+  a.hx = (P)(a.ox + a.Lx); a.hy = (P)(a.oy + a.Ly); a.hz = (P)(a.oz + a.Lz);
+  a.hx2 = (P)(a.hx + a.hx); a.hy2 = (P)(a.hy + a.hy); a.hz2 = (P)(a.hz + a.hz);
+  a.gdx = (F)c.geo_g[0]; a.gdy = (F)c.geo_g[1]; a.gdz = (F)c.geo_g[2];
+  a.gox = (F)c.geo_g[3]; a.goy = (F)c.geo_g[4]; a.goz = (F)c.geo_g[5];
+  a.nx = (int)c.geo_i[0]; a.ny = (int)c.geo_i[1]; a.nz = (int)c.geo_i[2];
+  a.bcx = (int)c.geo_i[3]; a.bcy = (int)c.geo_i[4]; a.bcz = (int)c.geo_i[5];
+  a.NY = a.ny + 1; a.NZ = a.nz + 1;
+  a.NN = (a.nx + 1) * a.NY * a.NZ;
+  a.dt = (P)c.dt; a.dth = (P)c.dth; a.qdt2m = (P)c.qdt2m; a.beta = (P)c.beta;
+  a.one = (P)c.one;
+  a.two = (P)(a.one + a.one);
+  a.beta2 = (P)(a.beta * a.beta);  // f32*f32 stays f32 (kernels.py:615)
+  a.scale = (F)c.scale;
+  a.n_iters = c.n_iters; a.mixed = c.mixed; a.apply_bc = c.apply_bc;
+  a.status = c.status;
+  a.gather_out = (P*)c.out;
+  return a;
+}
+
+constexpr int kThreads = 256;
+constexpr size_t kSmem = (size_t)(kThreads / 32) * kWarpScratch * sizeof(i64);
+
+template <typename K>
+int grid_for(K kernel, size_t smem, int64_t count) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (count + kThreads - 1) / kThreads;
+  const int64_t full = (int64_t)sms * per_sm;
+  return (int)(need < full ? need : full);
+}
+
+template <typename P, typename F, bool PUSH, bool DEP>
+int run_span(const Call& c, cudaStream_t s) {
+  auto a = make_params<P, F>(c);
+  auto k = span_kernel<P, F, PUSH, DEP>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    attr = true;
+  }
+  const int grid = grid_for(k, kSmem, c.count);
+  k<<<grid, kThreads, kSmem, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("span kernel launch: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+template <typename P, typename F>
+int run_gather(const Call& c, cudaStream_t s) {
+  auto a = make_params<P, F>(c);
+  const int grid = grid_for(gather_kernel<P, F>, 0, c.count);
+  gather_kernel<P, F><<<grid, kThreads, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("gather kernel launch: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+template <typename P, typename F>
+int dispatch(const Call& c, cudaStream_t s) {
+  switch (c.op) {
+    case OP_FUSED: return run_span<P, F, true, true>(c, s);
+    case OP_PUSH: return run_span<P, F, true, false>(c, s);
+    case OP_DEPOSIT: return run_span<P, F, false, true>(c, s);
+    case OP_GATHER: return run_gather<P, F>(c, s);
+  }
+  set_error("unknown op %d", c.op);
+  return -1;
+}
+
+}  // namespace
+
+int launch_parity(const Call& c, cudaStream_t s) {
+  if (c.pbytes == 8 && c.fbytes == 8) return dispatch<double, double>(c, s);
+  if (c.pbytes == 4 && c.fbytes == 4) return dispatch<float, float>(c, s);
+  if (c.pbytes == 4 && c.fbytes == 8) return dispatch<float, double>(c, s);
+  set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", c.pbytes,
+            c.fbytes);
+  return -1;
+}
+
+}  // namespace bp

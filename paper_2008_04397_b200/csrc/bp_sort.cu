@@ -1,0 +1,213 @@
+// On-device cell sort (particles.sort_by_cell, particles.py:157-167) and the
+// exact periodic fold of int64 moment grids (fields.fold_periodic,
+// fields.py:28-47).
+//
+// Sort: key kernel (geometry.cell_index_of semantics, geometry.py:152-159:
+// f64 arithmetic, truncation, clamp of the upper face, x fastest), a stable
+// LSD radix sort of (key, index) pairs over ceil(log2(n_cells)) bits, then a
+// gather-permute of the 8 particle arrays through one scratch array.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdint>
+
+#include "bp_launch.h"
+
+namespace bp {
+
+namespace {
+
+template <typename P>
+__global__ void cell_key_kernel(const P* __restrict__ x, const P* __restrict__ y,
+                                const P* __restrict__ z, int64_t n, double ox, double oy,
+                                double oz, double dx, double dy, double dz, int64_t nx,
+                                int64_t ny, int64_t nz, uint32_t* keys32, int64_t* keys64,
+                                uint32_t* idx, int* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    int64_t i = (int64_t)(((double)x[p] - ox) / dx);
+    int64_t j = (int64_t)(((double)y[p] - oy) / dy);
+    int64_t k = (int64_t)(((double)z[p] - oz) / dz);
+    i = i < nx - 1 ? i : nx - 1;
+    j = j < ny - 1 ? j : ny - 1;
+    k = k < nz - 1 ? k : nz - 1;
+    if (i < 0 || j < 0 || k < 0) {
+      *bad = 1;
+      i = j = k = 0;
+    }
+    const int64_t key = i + nx * (j + ny * k);
+    if (keys32) keys32[p] = (uint32_t)key;
+    if (keys64) keys64[p] = key;
+    if (idx) idx[p] = (uint32_t)p;
+  }
+}
+
+template <typename T>
+__global__ void gather_perm(const T* __restrict__ src, const uint32_t* __restrict__ order,
+                            T* __restrict__ dst, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
+    dst[r] = src[order[r]];
+}
+
+// fold one periodic axis of a (rows, NX, NY, NZ) grid: first += last; last = first
+__global__ void fold_axis(long long* a, int64_t rows, int NX, int NY, int NZ, int axis) {
+  const int n1 = axis == 0 ? NY : NX;
+  const int n2 = axis == 2 ? NY : NZ;
+  const int64_t plane = (int64_t)n1 * n2;
+  const int64_t total = rows * plane;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int64_t r = t / plane;
+    const int64_t rem = t - r * plane;
+    const int a1 = (int)(rem / n2), a2 = (int)(rem % n2);
+    int64_t first, last;
+    const int64_t base = r * (int64_t)NX * NY * NZ;
+    if (axis == 0) {
+      first = base + ((int64_t)0 * NY + a1) * NZ + a2;
+      last = base + ((int64_t)(NX - 1) * NY + a1) * NZ + a2;
+    } else if (axis == 1) {
+      first = base + ((int64_t)a1 * NY + 0) * NZ + a2;
+      last = base + ((int64_t)a1 * NY + (NY - 1)) * NZ + a2;
+    } else {
+      first = base + ((int64_t)a1 * NY + a2) * NZ + 0;
+      last = base + ((int64_t)a1 * NY + a2) * NZ + (NZ - 1);
+    }
+    const long long s = a[first] + a[last];
+    a[first] = s;
+    a[last] = s;
+  }
+}
+
+int blocks_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+int check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+template <typename P>
+int keys_launch(const void* xs, const void* ys, const void* zs, int64_t n, const double* o,
+                const double* d, const int64_t* c, uint32_t* k32, int64_t* k64, uint32_t* idx,
+                int* bad, cudaStream_t s) {
+  cell_key_kernel<P><<<blocks_for(n), 256, 0, s>>>((const P*)xs, (const P*)ys, (const P*)zs, n,
+                                                   o[0], o[1], o[2], d[0], d[1], d[2], c[0],
+                                                   c[1], c[2], k32, k64, idx, bad);
+  return check(cudaGetLastError(), "cell_key_kernel");
+}
+
+int keys_any(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+             const double* o, const double* d, const int64_t* c, uint32_t* k32, int64_t* k64,
+             uint32_t* idx, int* bad, cudaStream_t s) {
+  if (pbytes == 8) return keys_launch<double>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s);
+  if (pbytes == 4) return keys_launch<float>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s);
+  set_error("unsupported particle dtype (%d bytes)", pbytes);
+  return -1;
+}
+
+template <typename T>
+int permute_one(void* arr, const uint32_t* order, void* tmp, int64_t n, cudaStream_t s) {
+  gather_perm<T><<<blocks_for(n), 256, 0, s>>>((const T*)arr, order, (T*)tmp, n);
+  int rc = check(cudaGetLastError(), "gather_perm");
+  if (rc) return rc;
+  return check(cudaMemcpyAsync(arr, tmp, n * sizeof(T), cudaMemcpyDeviceToDevice, s),
+               "permute copy");
+}
+
+}  // namespace
+
+int cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+              const double* origin, const double* spacing, const int64_t* counts,
+              int64_t* keys, cudaStream_t s) {
+  if (n <= 0) return 0;
+  int* bad = nullptr;
+  int rc = check(cudaMallocAsync((void**)&bad, sizeof(int), s), "alloc");
+  if (rc) return rc;
+  cudaMemsetAsync(bad, 0, sizeof(int), s);
+  rc = keys_any(pbytes, xs, ys, zs, n, origin, spacing, counts, nullptr, keys, nullptr, bad, s);
+  int hbad = 0;
+  if (!rc) rc = check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
+  cudaFreeAsync(bad, s);
+  if (rc) return rc;
+  return hbad ? 3 : 0;
+}
+
+int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, void* ws,
+                 void* qs, int64_t* ids, int64_t n, const double* origin,
+                 const double* spacing, const int64_t* counts, cudaStream_t s) {
+  if (n <= 1) return 0;
+  if (n > 0xffffffffLL) {
+    set_error("sort_by_cell: %lld particles exceed the 32-bit index space", (long long)n);
+    return -1;
+  }
+  const int64_t ncell = counts[0] * counts[1] * counts[2];
+  int end_bit = 1;
+  while (end_bit < 32 && (1LL << end_bit) < ncell) ++end_bit;
+  uint32_t *k_in, *k_out, *i_in, *i_out;
+  int* bad;
+  void* tmp;
+  const size_t nb = (size_t)n * sizeof(uint32_t);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, end_bit, s);
+  void* cub_tmp;
+  int rc = 0;
+  rc |= check(cudaMallocAsync((void**)&k_in, nb, s), "alloc");
+  rc |= check(cudaMallocAsync((void**)&k_out, nb, s), "alloc");
+  rc |= check(cudaMallocAsync((void**)&i_in, nb, s), "alloc");
+  rc |= check(cudaMallocAsync((void**)&i_out, nb, s), "alloc");
+  rc |= check(cudaMallocAsync((void**)&bad, sizeof(int), s), "alloc");
+  rc |= check(cudaMallocAsync(&tmp, (size_t)n * 8, s), "alloc");
+  rc |= check(cudaMallocAsync(&cub_tmp, cub_bytes, s), "alloc");
+  if (rc) return -2;
+  cudaMemsetAsync(bad, 0, sizeof(int), s);
+  rc = keys_any(pbytes, xs, ys, zs, n, origin, spacing, counts, k_in, nullptr, i_in, bad, s);
+  int hbad = 0;
+  if (!rc) rc = check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
+  if (!rc && !hbad) {
+    rc = check(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k_in, k_out, i_in, i_out, n,
+                                               0, end_bit, s),
+               "radix sort");
+    void* parr[7] = {xs, ys, zs, us, vs, ws, qs};
+    for (int a = 0; a < 7 && !rc; ++a) {
+      if (!parr[a]) continue;
+      rc = pbytes == 8 ? permute_one<double>(parr[a], i_out, tmp, n, s)
+                       : permute_one<float>(parr[a], i_out, tmp, n, s);
+    }
+    if (!rc && ids) rc = permute_one<long long>(ids, i_out, tmp, n, s);
+    if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
+  }
+  cudaFreeAsync(k_in, s);
+  cudaFreeAsync(k_out, s);
+  cudaFreeAsync(i_in, s);
+  cudaFreeAsync(i_out, s);
+  cudaFreeAsync(bad, s);
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(cub_tmp, s);
+  if (rc) return rc;
+  return hbad ? 3 : 0;
+}
+
+int fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, cudaStream_t s) {
+  const int NX = (int)geo_i[0] + 1, NY = (int)geo_i[1] + 1, NZ = (int)geo_i[2] + 1;
+  for (int axis = 0; axis < 3; ++axis) {
+    if (geo_i[3 + axis] != 0) continue;  // reflecting
+    const int n1 = axis == 0 ? NY : NX;
+    const int n2 = axis == 2 ? NY : NZ;
+    fold_axis<<<blocks_for(rows * n1 * n2), 256, 0, s>>>((long long*)acc, rows, NX, NY, NZ, axis);
+    int rc = check(cudaGetLastError(), "fold_axis");
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // namespace bp

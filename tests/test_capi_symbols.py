@@ -1,0 +1,43 @@
+"""The C-ABI library builds, loads without a GPU and exports every entry
+point include/bp_b200.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+from conftest import ROOT
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "bp_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(bp_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    assert "bp_fused_span" in names and "bp_sort_by_cell" in names
+    from paper_2008_04397_b200 import _lib
+    assert sorted(_lib.EXPORTS) == names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2008_04397_b200 import _lib
+    lib = _lib.load()
+    raw = ctypes.CDLL(_lib.LIB_PATH)
+    for name in _declared():
+        assert hasattr(raw, name), name
+    assert lib.bp_version() >= 100
+    assert lib.bp_last_error() == b""
+
+
+def test_kernel_objects_are_sm100a():
+    # the fatbin carries sm_100a SASS (cuobjdump lists the ELF arch)
+    import shutil
+    import subprocess
+    from paper_2008_04397_b200 import _lib
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        return
+    out = subprocess.run([exe, "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out

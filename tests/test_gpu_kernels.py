@@ -1,0 +1,160 @@
+"""CUDA kernels through the C ABI against the reference golden vectors and the
+CPU oracle: bitwise in parity arithmetic for double / single / mixed."""
+
+import numpy as np
+import pytest
+
+from conftest import MODES, golden
+from test_oracle_golden import case_args
+
+pytestmark = pytest.mark.gpu
+
+SCALE = 2.0 ** 43
+
+
+def _dev(torch, arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("ci", [0, 1, 2])
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_fused_matches_reference_golden(gpu, mode, ci, where):
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    g = golden(f"kernels_{mode}.npz")
+    a = case_args(g, mode, ci)
+    acc = np.zeros((10, 9, 9, 9), np.int64)
+    args = (a["start"], a["count"])
+    tail = (a["geo_f"], a["geo_g"], a["geo_i"], a["sc"]["dt"], a["sc"]["dth"],
+            a["sc"]["qdt2m"], a["sc"]["beta"], a["sc"]["one"], 3, a["fd"](SCALE),
+            a["mixed"])
+    if where == "device":
+        d = _dev(torch, a["arrs"])
+        dE, dB, dacc, dinv = _dev(torch, [a["E"], a["B"], acc, a["inv"]])
+        st = K.fused_span(*d, *args, dE, dB, dacc, dinv, *tail)
+        out = [t.cpu().numpy() for t in d]
+        acc = dacc.cpu().numpy()
+    else:
+        out = a["arrs"]
+        st = K.fused_span(*out, *args, a["E"], a["B"], acc, a["inv"], *tail,
+                          batch_particles=1000)
+    assert st == int(g[a["pre"] + "fused_status"])
+    for n, arr in zip("xyzuvw", out):
+        assert np.array_equal(arr, g[a["pre"] + "fused_" + n]), n
+    assert np.array_equal(acc, g[a["pre"] + "fused_acc"])
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("ci", [0, 2])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_push_matches_reference_golden(gpu, mode, ci, bc):
+    from paper_2008_04397_b200 import kernels as K
+    g = golden(f"kernels_{mode}.npz")
+    a = case_args(g, mode, ci)
+    arrs = a["arrs"][:6]
+    st = K.push_span(*arrs, a["start"], a["count"], a["E"], a["B"], a["geo_f"],
+                     a["geo_g"], a["geo_i"], a["sc"]["dt"], a["sc"]["dth"],
+                     a["sc"]["qdt2m"], a["sc"]["beta"], a["sc"]["one"], 3, bc,
+                     a["mixed"])
+    assert st == int(g[a["pre"] + f"push{bc}_status"])
+    for n, arr in zip("xyzuvw", arrs):
+        assert np.array_equal(arr, g[a["pre"] + f"push{bc}_" + n]), n
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("ci", [0, 1])
+def test_deposit_and_gather_match_reference_golden(gpu, mode, ci):
+    from paper_2008_04397_b200 import kernels as K
+    g = golden(f"kernels_{mode}.npz")
+    a = case_args(g, mode, ci)
+    acc = np.zeros((10, 9, 9, 9), np.int64)
+    st = K.deposit_span(*a["arrs"], a["start"], a["count"], acc, a["inv"], a["geo_g"],
+                        a["geo_i"], a["fd"](1.0), a["fd"](SCALE))
+    assert st == 0
+    assert np.array_equal(acc, g[a["pre"] + "deposit_acc"])
+    out = np.zeros((a["count"], 6), a["pd"])
+    K.gather_span(a["arrs"][0], a["arrs"][1], a["arrs"][2], a["start"], a["count"],
+                  a["E"], a["B"], a["geo_g"], a["geo_i"], a["pd"](1.0), out)
+    assert np.array_equal(out, g[a["pre"] + "gather_out"])
+
+
+def _random_state(mode, n, seed, cells=(16, 8, 8), box=(6.4, 3.2, 3.2), vscale=0.3,
+                  order="random"):
+    from paper_2008_04397_b200.geometry import GridGeometry
+    from paper_2008_04397_b200 import kernels as K
+    from paper_2008_04397_b200.config import SpeciesParams
+    pd, fd = MODES[mode]
+    geom = GridGeometry.from_box(cells, box, bc=("periodic", "reflecting", "periodic"))
+    rng = np.random.default_rng(seed)
+    x = rng.random(n) * geom.Lx
+    y = rng.random(n) * geom.Ly
+    z = rng.random(n) * geom.Lz
+    if order == "sorted":
+        keys = geom.cell_index_of(x, y, z)
+        o = np.argsort(keys, kind="stable")
+        x, y, z = x[o], y[o], z[o]
+    arrs = [x.astype(pd), y.astype(pd), z.astype(pd)] + [
+        (rng.standard_normal(n) * vscale).astype(pd) for _ in range(3)] + [
+        (rng.random(n) * 1e-3 + 1e-4).astype(pd)]
+    shp = (3,) + geom.node_shape
+    E = (rng.standard_normal(shp) * 0.05).astype(fd)
+    B = (rng.standard_normal(shp) * 0.8).astype(fd)
+    sp = SpeciesParams(0, -1.0, 0.1, 1, mover_iters=3)
+    geo_f, geo_i = K.make_geo_arrays(geom, pd)
+    geo_g, _ = K.make_geo_arrays(geom, fd)
+    sc = K.kernel_scalars(sp, 0.2, 1.0, pd)
+    return geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("order", ["random", "sorted"])
+def test_fused_matches_oracle_large(gpu, oracle, mode, order):
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 400_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(
+        mode, n, seed=11, order=order)
+    inv = geom.inv_node_volume(fd)
+    mixed = 1 if pd != fd else 0
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    ref = [a.copy() for a in arrs]
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"],
+            sc["one"], 3, fd(SCALE), mixed)
+    st_ref = oracle.fused_span(*ref, 0, n, E, B, acc_ref, inv, *tail)
+    d = _dev(torch, arrs)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    st = K.fused_span(*d, 0, n, dE, dB, dacc, dinv, *tail)
+    assert st == st_ref
+    for name, r, t in zip("xyzuvw", ref, d):
+        assert np.array_equal(r, t.cpu().numpy()), name
+    assert np.array_equal(acc_ref, dacc.cpu().numpy())
+
+
+def test_fused_empty_span_and_offsets(gpu, oracle):
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 5000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state("double", n, 3)
+    inv = geom.inv_node_volume(fd)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"],
+            sc["one"], 3, SCALE, 0)
+    d = _dev(torch, arrs)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    before = [t.clone() for t in d]
+    assert K.fused_span(*d, 2500, 0, dE, dB, dacc, dinv, *tail) == 0
+    assert int(dacc.abs().sum()) == 0
+    assert all(torch.equal(a, b) for a, b in zip(before, d))
+    # two disjoint spans into one accumulator == one span
+    K.fused_span(*d, 0, 1234, dE, dB, dacc, dinv, *tail)
+    K.fused_span(*d, 1234, n - 1234, dE, dB, dacc, dinv, *tail)
+    ref = [a.copy() for a in arrs]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    oracle.fused_span(*ref, 0, n, E, B, acc_ref, inv, *tail)
+    assert np.array_equal(acc_ref, dacc.cpu().numpy())
+    for r, t in zip(ref, d):
+        assert np.array_equal(r, t.cpu().numpy())
+    with pytest.raises(IndexError):
+        K.fused_span(*d, n - 10, 11, dE, dB, dacc, dinv, *tail)
