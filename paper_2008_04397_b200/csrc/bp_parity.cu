@@ -1,6 +1,7 @@
 // Parity build of the span kernels: compiled with -fmad=false and IEEE
 // division so every particle follows the reference numba arithmetic bit for
 // bit (kernels.py:458-735).
+#include <cmath>
 #include <cstdio>
 
 #include "bp_launch.h"
@@ -39,11 +40,22 @@ SpanParams<P, F> make_params(const Call& c) {
   a.n_iters = c.n_iters; a.mixed = c.mixed; a.apply_bc = c.apply_bc;
   a.status = c.status;
   a.gather_out = (P*)c.out;
+  const P o3[3] = {a.ox, a.oy, a.oz}, L3[3] = {a.Lx, a.Ly, a.Lz};
+  const P h3[3] = {a.hx, a.hy, a.hz}, h23[3] = {a.hx2, a.hy2, a.hz2};
+  const F gd3[3] = {a.gdx, a.gdy, a.gdz}, go3[3] = {a.gox, a.goy, a.goz};
+  for (int k = 0; k < 3; ++k) {
+    a.d.o[k] = (double)o3[k]; a.d.L[k] = (double)L3[k];
+    a.d.hi[k] = (double)h3[k]; a.d.hi2[k] = (double)h23[k];
+    a.d.gd[k] = (double)gd3[k]; a.d.go[k] = (double)go3[k];
+  }
+  a.d.dt = (double)a.dt; a.d.dth = (double)a.dth; a.d.qdt2m = (double)a.qdt2m;
+  a.d.beta = (double)a.beta; a.d.one = (double)a.one; a.d.two = (double)a.two;
+  a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
   return a;
 }
 
 constexpr int kThreads = 256;
-constexpr size_t kSmem = (size_t)(kThreads / 32) * kWarpScratch * sizeof(i64);
+constexpr size_t kSmem = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
 
 template <typename K>
 int grid_for(K kernel, size_t smem, int64_t count) {
@@ -61,16 +73,20 @@ int grid_for(K kernel, size_t smem, int64_t count) {
   return (int)(need < full ? need : full);
 }
 
-template <typename P, typename F, bool PUSH, bool DEP>
-int run_span(const Call& c, cudaStream_t s) {
-  auto a = make_params<P, F>(c);
-  auto k = span_kernel<P, F, PUSH, DEP>;
+bool is_pow2(double v) {
+  int e;
+  return v > 0.0 && std::isfinite(v) && std::frexp(v, &e) == 0.5;
+}
+
+template <typename P, typename F, bool PUSH, bool DEP, bool PRE>
+int launch_span(const SpanParams<P, F>& a, int64_t count, cudaStream_t s) {
+  auto k = span_kernel<P, F, PUSH, DEP, PRE>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     attr = true;
   }
-  const int grid = grid_for(k, kSmem, c.count);
+  const int grid = grid_for(k, kSmem, count);
   k<<<grid, kThreads, kSmem, s>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -78,6 +94,29 @@ int run_span(const Call& c, cudaStream_t s) {
     return -2;
   }
   return 0;
+}
+
+template <typename P, typename F, bool PUSH, bool DEP>
+int run_span(const Call& c, cudaStream_t s) {
+  auto a = make_params<P, F>(c);
+  // per-call node records (E, B, invvol widened to double), stream-ordered
+  double* fn = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&fn, (size_t)a.NN * 8 * sizeof(double), s);
+  if (e != cudaSuccess) {
+    set_error("node record alloc: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
+  pack_nodes<F><<<pb, 256, 0, s>>>(PUSH ? a.E : nullptr, PUSH ? a.B : nullptr,
+                                   DEP ? a.invvol : nullptr, a.NN, fn);
+  a.fnode = fn;
+  int rc;
+  if (DEP && is_pow2(c.scale))
+    rc = launch_span<P, F, PUSH, DEP, true>(a, c.count, s);
+  else
+    rc = launch_span<P, F, PUSH, DEP, false>(a, c.count, s);
+  cudaFreeAsync(fn, s);
+  return rc;
 }
 
 template <typename P, typename F>
