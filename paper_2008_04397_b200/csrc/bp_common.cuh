@@ -1,0 +1,369 @@
+// Fused implicit mover + moment deposition, sm_100a — shared machinery.
+//
+// Semantics follow the reference batchpic kernels (pkg/src/batchpic/kernels.py):
+//   push block   fused_span :489-682 (== push_span :112-306)
+//   deposit      fused_span :683-734 (== deposit_span :327-381)
+//   gather       gather_span :385-455
+// The arithmetic of the push block and of the per-particle deposit values is
+// a policy: bp_parity_policy.cuh (bitwise the reference, compiled with
+// -fmad=false) or bp_fast_policy.cuh (FMA, reciprocals, native f32).  The
+// kernel body, the field records and the exact deposition are shared here.
+//
+// Layout in HBM (the reference data contract, unchanged):
+//   particles  SoA x y z u v w q, one contiguous array each (P)
+//   E, B       (3, nx+1, ny+1, nz+1) C order, k fastest (F)
+//   acc        (10, nx+1, ny+1, nz+1) int64 fixed point (rho Jx Jy Jz Pxx Pxy
+//              Pxz Pyy Pyz Pzz), quantum 2^-43 (fields.py:20-25)
+//   invvol     (nx+1, ny+1, nz+1) (F)
+// plus one per-call scratch array of node records (pack_nodes).
+//
+// Deposition is exact integer arithmetic, so contributions may be summed in
+// any grouping: per-cell sums are kept in registers spread over a warp and
+// flushed with one REDG.ADD.64 per (node, moment) when the cell changes; the
+// result is bit-identical to the reference's sequential `acc[...] += rint(...)`.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bp {
+
+typedef long long i64;
+typedef unsigned long long u64;  // modular sums of biased bit patterns
+
+// ST_DOMAIN: a deposit/gather position outside the box (the reference does
+// not check; the GPU refuses to index out of bounds).
+enum { ST_OK = 0, ST_RUNAWAY = 1, ST_MIDPOINT = 2, ST_DOMAIN = 3 };
+
+// Scalars widened to double once on the host (exact), so kernels never
+// re-convert them per particle; inv_gd / go_s serve the fast arithmetic
+// only (gx = x * (1/d) - o/d).
+struct WideScalars {
+  double o[3], L[3], hi[3], hi2[3], gd[3], go[3], inv_gd[3], go_s[3];
+  double dt, dth, qdt2m, beta, one, two, beta2, scale;
+};
+
+template <typename P, typename F>
+struct SpanParams {
+  P *x, *y, *z, *u, *v, *w;
+  const P* q;
+  i64 start, count;
+  const F* E;
+  const F* B;
+  i64* acc;
+  const F* invvol;
+  // boundary arithmetic (particle precision), hi = (P)(o + L), hi2 = (P)(hi + hi)
+  P ox, oy, oz, Lx, Ly, Lz, hx, hy, hz, hx2, hy2, hz2;
+  // cell location (field precision)
+  F gdx, gdy, gdz, gox, goy, goz;
+  int nx, ny, nz, bcx, bcy, bcz;
+  int NY, NZ, NN;  // node extents (y, z) and node count
+  P dt, dth, qdt2m, beta, one, two, beta2;
+  F scale;
+  WideScalars d;
+  int n_iters, mixed, apply_bc;
+  int* status;
+  P* gather_out;  // gather only: (count, 6)
+  // per-call node records (pack_nodes), element type Policy::NodeT:
+  // Ex Ey Ez Bx By Bz invvol 0 for every node
+  const void* fnode;
+};
+
+__device__ __forceinline__ unsigned lane_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
+}
+
+// E, B, invvol -> one 8-element record per node, so one corner of a gather is
+// a couple of 16-byte loads from one record and the deposit's control volume
+// comes from the same line.  T = double (parity: exact widening) or the fast
+// policy's compute type.
+template <typename F, typename T>
+__global__ void pack_nodes(const F* __restrict__ E, const F* __restrict__ B,
+                           const F* __restrict__ invvol, int NN, T* __restrict__ out) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < NN; n += stride) {
+    T r[8];
+    r[0] = E ? (T)E[n] : T(0);
+    r[1] = E ? (T)E[NN + n] : T(0);
+    r[2] = E ? (T)E[2 * NN + n] : T(0);
+    r[3] = B ? (T)B[n] : T(0);
+    r[4] = B ? (T)B[NN + n] : T(0);
+    r[5] = B ? (T)B[2 * NN + n] : T(0);
+    r[6] = invvol ? (T)invvol[n] : T(0);
+    r[7] = T(0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out[(size_t)n * 8 + k] = r[k];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Deposition.  Contribution (moment m, corner c) of one particle is
+//   rint((base_c * m) * scale),  base_c = (q * (wx*wy*wz)) * invvol_c
+// (kernels.py:707-734), m in {1, u, v, w, uu, uv, uw, vv, vw, ww}.  The
+// policy stages per particle the 8 bases (pre-multiplied by scale when that
+// is exact — PRESCALE) and the 10 moment values as doubles.
+//
+// Each warp walks a contiguous run of (cell-sorted) particles; the 80 sums
+// of the cell currently being filled live in registers spread over the 32
+// lanes: lane L owns corner c = L & 7 of moments g, g+4, g+8 (g = L >> 3).
+// Per tile of 32 particles the owning lanes stage their values in shared
+// memory, then all lanes fold every particle into their 2-3 accumulators —
+// no cross-lane reduction at all.  A second slot keeps the sums of the last
+// "stray" cell (a particle that crossed into a neighbour cell, or the next
+// cell of the sort) so it does not force a flush of the main cell.  Sums are
+// flushed with one REDG.ADD.64 per (slot, value) when a slot is evicted.
+
+__device__ __forceinline__ void red_add(i64* p, i64 v) {
+  if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+// shared-memory staging of one warp (doubles): bases [32][8] and moments
+// [32][4][4] laid out so lane group g reads (m_g, m_g+4) with one 16-byte
+// load and m_g+8 (zero for g >= 2) with a second
+constexpr int kStageBs = 32 * 8;
+constexpr int kStageMv = 32 * 16;
+constexpr int kWarpStage = kStageBs + kStageMv + 16;  // + 32 int keys
+
+// Exact rint without the conversion pipe: for |t| < 2^51, t + 1.5*2^52 lands
+// in [2^52, 2^53) where the ulp is 1, so the FP add rounds t half-to-even
+// exactly like cvt.rni and the low mantissa bits hold rint(t) in two's
+// complement: bits(t + M) = bits(M) + rint(t).  Slots accumulate raw bit
+// patterns and subtract n * bits(M) when flushed.  Tiles whose values could
+// leave the range take the cvt path instead (checked per particle).
+// FMA = true (fast policy only) rounds the exact product b*m instead of
+// RN(b*m) — one rounding less, not bitwise the reference.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr i64 kMagicBits = 0x4338000000000000LL;
+constexpr double kMagicLimit = 1125899906842624.0;  // 2^50
+
+struct Slot {
+  int key;
+  int n;  // folded particles since the last flush (bit-pattern bias count)
+  u64 s0, s1, s2;
+};
+
+__device__ __forceinline__ void slot_flush(const Slot& sl, i64* __restrict__ acc, int NN,
+                                           int m0, int coff, bool third) {
+  if (sl.key < 0) return;
+  const u64 bias = (u64)sl.n * (u64)kMagicBits;
+  i64* p = acc + (size_t)m0 * NN + sl.key + coff;
+  red_add(p, (i64)(sl.s0 - bias));
+  red_add(p + (size_t)4 * NN, (i64)(sl.s1 - bias));
+  if (third) red_add(p + (size_t)8 * NN, (i64)(sl.s2 - bias));
+}
+
+// quantised value as a biased bit pattern: bits(M) + rint(t)
+template <bool PRESCALE, bool MAGIC, bool FMA>
+__device__ __forceinline__ u64 qbits(double b, double m, double sc) {
+  if (MAGIC) {
+    if (FMA) return (u64)__double_as_longlong(__fma_rn(b, m, kMagic));
+    const double t = PRESCALE ? b * m : b * m * sc;
+    return (u64)__double_as_longlong(t + kMagic);
+  }
+  const double t = PRESCALE ? b * m : b * m * sc;
+  return (u64)__double2ll_rn(t) + (u64)kMagicBits;
+}
+
+template <bool PRESCALE, bool MAGIC, bool FMA>
+__device__ __forceinline__ void fold_vals(u64& s0, u64& s1, u64& s2, const double* st_bs,
+                                          const double* st_mv, int k, int lc, int lg,
+                                          double sc) {
+  const double b = st_bs[k * 8 + lc];
+  const double2 m01 = *reinterpret_cast<const double2*>(st_mv + k * 16 + lg * 4);
+  const double m2 = st_mv[k * 16 + lg * 4 + 2];
+  s0 += qbits<PRESCALE, MAGIC, FMA>(b, m01.x, sc);
+  s1 += qbits<PRESCALE, MAGIC, FMA>(b, m01.y, sc);
+  s2 += qbits<PRESCALE, MAGIC, FMA>(b, m2, sc);  // m2 == 0 for lane groups 2, 3
+}
+
+template <bool PRESCALE, bool MAGIC, bool FMA>
+__device__ __forceinline__ void fold_one(Slot& S, const double* st_bs, const double* st_mv,
+                                         int k, int lc, int lg, double sc) {
+  fold_vals<PRESCALE, MAGIC, FMA>(S.s0, S.s1, S.s2, st_bs, st_mv, k, lc, lg, sc);
+  S.n += 1;
+}
+
+// all 32 staged particles into S, two interleaved chains
+template <bool PRESCALE, bool MAGIC, bool FMA>
+__device__ __forceinline__ void fold_tile(Slot& S, const double* st_bs, const double* st_mv,
+                                          int lc, int lg, double sc) {
+  u64 t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll 8
+  for (int k = 0; k < 32; k += 2) {
+    fold_vals<PRESCALE, MAGIC, FMA>(S.s0, S.s1, S.s2, st_bs, st_mv, k, lc, lg, sc);
+    fold_vals<PRESCALE, MAGIC, FMA>(t0, t1, t2, st_bs, st_mv, k + 1, lc, lg, sc);
+  }
+  S.s0 += t0; S.s1 += t1; S.s2 += t2;
+  S.n += 32;
+}
+
+// Stage the moment values m0..m9 = 1 u v w uu uv uw vv vw ww of one particle,
+// grouped (g, g+4, g+8) per lane group.
+__device__ __forceinline__ void stage_moments(double* mv, double u, double v, double w,
+                                              double uu, double uv, double uw, double vv,
+                                              double vw, double ww) {
+  double2* m2 = reinterpret_cast<double2*>(mv);
+  m2[0] = make_double2(1.0, uu);
+  m2[1] = make_double2(vw, 0.0);
+  m2[2] = make_double2(u, uv);
+  m2[3] = make_double2(ww, 0.0);
+  m2[4] = make_double2(v, uw);
+  m2[5] = make_double2(0.0, 0.0);
+  m2[6] = make_double2(w, vv);
+  m2[7] = make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ void stage_bases(double* st, const double bs[8]) {
+  double2* b2 = reinterpret_cast<double2*>(st);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) b2[c] = make_double2(bs[2 * c], bs[2 * c + 1]);
+}
+
+// |value| < 2^50 for every (corner, moment) keeps the magic rint exact
+__device__ __forceinline__ bool magic_unsafe(const double bs[8], double u, double v, double w,
+                                             double uu, double vv, double ww, double lim) {
+  double mb = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) mb = fmax(mb, fabs(bs[c]));
+  double mm = fmax(1.0, fmax(fabs(u), fmax(fabs(v), fabs(w))));
+  mm = fmax(mm, fmax(uu, fmax(vv, ww)));
+  return !(mb * mm < lim);
+}
+
+// Fold one staged tile into the slots.  Lanes are grouped by cell with
+// ballots: the group of the main slot's cell (usually almost the whole warp)
+// and, one by one, the few other cells present, which go through the stray
+// slot; strays then have their bases zeroed so the main fold runs unmasked
+// over all 32 (invalid lanes staged zero bases too).
+template <bool PRESCALE, bool FMA>
+__device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict__ acc, int NN,
+                                             int key, bool big, double* st_bs,
+                                             const double* st_mv, unsigned lane, int lc,
+                                             int lg, int coff, bool third, double sc) {
+  const bool has = key >= 0;
+  const unsigned V = __ballot_sync(0xffffffffu, has);
+  const bool magic = __ballot_sync(0xffffffffu, big) == 0u;
+  if (V == 0u) return;
+  unsigned MA = __ballot_sync(0xffffffffu, has && key == A.key);
+  if (MA == 0u) {
+    const int knew = __shfl_sync(0xffffffffu, key, __ffs(V) - 1);
+    if (knew == Bs.key) {
+      const Slot t = A;
+      A = Bs;
+      Bs = t;
+    } else {
+      slot_flush(Bs, acc, NN, lg, coff, third);
+      Bs = A;
+      A.key = knew;
+      A.n = 0;
+      A.s0 = A.s1 = A.s2 = 0;
+    }
+    MA = __ballot_sync(0xffffffffu, has && key == A.key);
+  }
+  const unsigned strays = V & ~MA;
+  unsigned rest = strays;
+  while (rest) {
+    const int k2 = __shfl_sync(0xffffffffu, key, __ffs(rest) - 1);
+    const unsigned M2 = __ballot_sync(0xffffffffu, has && key == k2);
+    rest &= ~M2;
+    if (k2 != Bs.key) {
+      slot_flush(Bs, acc, NN, lg, coff, third);
+      Bs.key = k2;
+      Bs.n = 0;
+      Bs.s0 = Bs.s1 = Bs.s2 = 0;
+    }
+    if (magic) {
+      for (unsigned m = M2; m; m &= m - 1u)
+        fold_one<PRESCALE, true, FMA>(Bs, st_bs, st_mv, __ffs(m) - 1, lc, lg, sc);
+    } else {
+      for (unsigned m = M2; m; m &= m - 1u)
+        fold_one<PRESCALE, false, FMA>(Bs, st_bs, st_mv, __ffs(m) - 1, lc, lg, sc);
+    }
+  }
+  if (strays) {
+    if ((strays >> lane) & 1u) {
+      double2* b2 = reinterpret_cast<double2*>(st_bs + lane * 8);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b2[c] = make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+  }
+  if (magic)
+    fold_tile<PRESCALE, true, FMA>(A, st_bs, st_mv, lc, lg, sc);
+  else
+    fold_tile<PRESCALE, false, FMA>(A, st_bs, st_mv, lc, lg, sc);
+}
+
+// --------------------------------------------------------------------------
+// One kernel body for fused / push-only / deposit-only.  Each warp owns a
+// contiguous run of the span and walks it 32 particles at a time (coalesced
+// SoA loads/stores); every lane of a warp runs the same trip count so warp
+// collectives always see 32 lanes.
+//
+// Policy provides:  P, F, NodeT, kFmaFold,
+//   static int push(const Params&, P& x, P& y, P& z, P& u, P& v, P& w)
+//   static int stage(const Params&, bool valid, P x, P y, P z, P u, P v, P w,
+//                    P q, double* st_bs_lane, double* st_mv_lane, bool& big)
+//     -> cell key (node index of corner 000) or -1 when outside the box.
+template <class Pol, bool DO_PUSH, bool DO_DEPOSIT, bool PRESCALE>
+__global__ void __launch_bounds__(256, 2)
+    span_kernel(SpanParams<typename Pol::P, typename Pol::F> a) {
+  typedef typename Pol::P P;
+  extern __shared__ double stage_all[];
+  const unsigned lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  const i64 nwarps = (i64)gridDim.x * (blockDim.x >> 5);
+  const i64 gw = (i64)blockIdx.x * (blockDim.x >> 5) + wib;
+  const i64 per = ((a.count + nwarps - 1) / nwarps + 31) & ~(i64)31;
+  const i64 w0 = gw * per;
+  const i64 w1 = w0 + per < a.count ? w0 + per : a.count;
+  double* const st_bs = stage_all + (size_t)wib * kWarpStage;
+  double* const st_mv = st_bs + kStageBs;
+  const int sx = a.NY * a.NZ, sy = a.NZ;
+  // this lane's share of the 80 sums
+  const int lc = lane & 7, lg = lane >> 3;
+  const int coff = (lc & 1) * sx + ((lc >> 1) & 1) * sy + ((lc >> 2) & 1);
+  const bool third = lg < 2;
+  const double sc = a.d.scale;
+  Slot A{-1, 0, 0, 0, 0}, Bs{-1, 0, 0, 0, 0};
+  int worst = ST_OK;
+  for (i64 t0 = w0; t0 < w1; t0 += 32) {
+    const i64 r = t0 + lane;
+    bool valid = r < w1;
+    const i64 p = a.start + r;
+    P xp = 0, yp = 0, zp = 0, un = 0, vn = 0, wn = 0, qp = 0;
+    if (valid) {
+      xp = a.x[p]; yp = a.y[p]; zp = a.z[p];
+      un = a.u[p]; vn = a.v[p]; wn = a.w[p];
+      if (DO_DEPOSIT) qp = a.q[p];
+    }
+    if (DO_PUSH && valid) {
+      const int st = Pol::push(a, xp, yp, zp, un, vn, wn);
+      if (st != ST_OK) {
+        worst = st > worst ? st : worst;
+        valid = false;
+      } else {
+        a.x[p] = xp; a.y[p] = yp; a.z[p] = zp;
+        a.u[p] = un; a.v[p] = vn; a.w[p] = wn;
+      }
+    }
+    if (DO_DEPOSIT) {
+      bool big = false;
+      const int key = Pol::template stage<PRESCALE>(a, valid, xp, yp, zp, un, vn, wn, qp,
+                                                    st_bs + lane * 8, st_mv + lane * 16, big);
+      if (valid && key < 0) worst = ST_DOMAIN > worst ? ST_DOMAIN : worst;
+      __syncwarp();
+      deposit_tile<PRESCALE, Pol::kFmaFold>(A, Bs, a.acc, a.NN, key, big, st_bs, st_mv, lane,
+                                            lc, lg, coff, third, sc);
+      __syncwarp();
+    }
+  }
+  if (DO_DEPOSIT) {
+    slot_flush(A, a.acc, a.NN, lg, coff, third);
+    slot_flush(Bs, a.acc, a.NN, lg, coff, third);
+  }
+  if (worst != ST_OK) atomicMax(a.status, worst);
+}
+
+}  // namespace bp

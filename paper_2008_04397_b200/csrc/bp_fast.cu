@@ -1,9 +1,33 @@
-// Fast-arithmetic build of the span kernels (placeholder until implemented).
-#include "bp_launch.h"
+// Fast build of the span kernels: FMA contraction, reciprocal multiplies and
+// native particle-precision arithmetic (bp_fast_policy.cuh).  Deposits keep
+// the exact int64 lattice.
+#include "bp_fast_policy.cuh"
+#include "bp_launch_impl.cuh"
+
 namespace bp {
-int launch_fast(const Call& c, cudaStream_t s) {
-  (void)c; (void)s;
-  set_error("fast arithmetic not available in this build");
+namespace {
+
+template <typename P, typename F>
+int dispatch(const Call& c, cudaStream_t s) {
+  typedef FastPolicy<P, F> Pol;
+  switch (c.op) {
+    case OP_FUSED: return run_span<Pol, true, true>(c, true, s);
+    case OP_PUSH: return run_span<Pol, true, false>(c, true, s);
+    case OP_DEPOSIT: return run_span<Pol, false, true>(c, true, s);
+  }
+  set_error("op %d has no fast arithmetic variant", c.op);
   return -1;
 }
+
+}  // namespace
+
+int launch_fast(const Call& c, cudaStream_t s) {
+  if (c.pbytes == 8 && c.fbytes == 8) return dispatch<double, double>(c, s);
+  if (c.pbytes == 4 && c.fbytes == 4) return dispatch<float, float>(c, s);
+  if (c.pbytes == 4 && c.fbytes == 8) return dispatch<float, double>(c, s);
+  set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", c.pbytes,
+            c.fbytes);
+  return -1;
+}
+
 }  // namespace bp

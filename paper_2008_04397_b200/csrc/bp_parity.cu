@@ -1,105 +1,15 @@
 // Parity build of the span kernels: compiled with -fmad=false and IEEE
 // division so every particle follows the reference numba arithmetic bit for
 // bit (kernels.py:458-735).
-#include <cmath>
-#include <cstdio>
-
-#include "bp_launch.h"
-#include "bp_span.cuh"
+#include "bp_launch_impl.cuh"
+#include "bp_parity_policy.cuh"
 
 namespace bp {
-
 namespace {
 
 template <typename P, typename F>
-SpanParams<P, F> make_params(const Call& c) {
-  SpanParams<P, F> a;
-  a.x = (P*)c.x; a.y = (P*)c.y; a.z = (P*)c.z;
-  a.u = (P*)c.u; a.v = (P*)c.v; a.w = (P*)c.w;
-  a.q = (const P*)c.q;
-  a.start = c.start; a.count = c.count;
-  a.E = (const F*)c.E; a.B = (const F*)c.B;
-  a.acc = (i64*)c.acc;
-  a.invvol = (const F*)c.invvol;
-  a.ox = (P)c.geo_f[3]; a.oy = (P)c.geo_f[4]; a.oz = (P)c.geo_f[5];
-  a.Lx = (P)c.geo_f[6]; a.Ly = (P)c.geo_f[7]; a.Lz = (P)c.geo_f[8];
-  // ox + Lx and (ox+Lx) + (ox+Lx) in particle precision (kernels.py:507-533)
-  a.hx = (P)(a.ox + a.Lx); a.hy = (P)(a.oy + a.Ly); a.hz = (P)(a.oz + a.Lz);
-  a.hx2 = (P)(a.hx + a.hx); a.hy2 = (P)(a.hy + a.hy); a.hz2 = (P)(a.hz + a.hz);
-  a.gdx = (F)c.geo_g[0]; a.gdy = (F)c.geo_g[1]; a.gdz = (F)c.geo_g[2];
-  a.gox = (F)c.geo_g[3]; a.goy = (F)c.geo_g[4]; a.goz = (F)c.geo_g[5];
-  a.nx = (int)c.geo_i[0]; a.ny = (int)c.geo_i[1]; a.nz = (int)c.geo_i[2];
-  a.bcx = (int)c.geo_i[3]; a.bcy = (int)c.geo_i[4]; a.bcz = (int)c.geo_i[5];
-  a.NY = a.ny + 1; a.NZ = a.nz + 1;
-  a.NN = (a.nx + 1) * a.NY * a.NZ;
-  a.dt = (P)c.dt; a.dth = (P)c.dth; a.qdt2m = (P)c.qdt2m; a.beta = (P)c.beta;
-  a.one = (P)c.one;
-  a.two = (P)(a.one + a.one);
-  a.beta2 = (P)(a.beta * a.beta);  // f32*f32 stays f32 (kernels.py:615)
-  a.scale = (F)c.scale;
-  a.n_iters = c.n_iters; a.mixed = c.mixed; a.apply_bc = c.apply_bc;
-  a.status = c.status;
-  a.gather_out = (P*)c.out;
-  const P o3[3] = {a.ox, a.oy, a.oz}, L3[3] = {a.Lx, a.Ly, a.Lz};
-  const P h3[3] = {a.hx, a.hy, a.hz}, h23[3] = {a.hx2, a.hy2, a.hz2};
-  const F gd3[3] = {a.gdx, a.gdy, a.gdz}, go3[3] = {a.gox, a.goy, a.goz};
-  for (int k = 0; k < 3; ++k) {
-    a.d.o[k] = (double)o3[k]; a.d.L[k] = (double)L3[k];
-    a.d.hi[k] = (double)h3[k]; a.d.hi2[k] = (double)h23[k];
-    a.d.gd[k] = (double)gd3[k]; a.d.go[k] = (double)go3[k];
-  }
-  a.d.dt = (double)a.dt; a.d.dth = (double)a.dth; a.d.qdt2m = (double)a.qdt2m;
-  a.d.beta = (double)a.beta; a.d.one = (double)a.one; a.d.two = (double)a.two;
-  a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
-  return a;
-}
-
-constexpr int kThreads = 256;
-constexpr size_t kSmem = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
-
-template <typename K>
-int grid_for(K kernel, size_t smem, int64_t count) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t need = (count + kThreads - 1) / kThreads;
-  const int64_t full = (int64_t)sms * per_sm;
-  return (int)(need < full ? need : full);
-}
-
-bool is_pow2(double v) {
-  int e;
-  return v > 0.0 && std::isfinite(v) && std::frexp(v, &e) == 0.5;
-}
-
-template <typename P, typename F, bool PUSH, bool DEP, bool PRE>
-int launch_span(const SpanParams<P, F>& a, int64_t count, cudaStream_t s) {
-  auto k = span_kernel<P, F, PUSH, DEP, PRE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    attr = true;
-  }
-  const int grid = grid_for(k, kSmem, count);
-  k<<<grid, kThreads, kSmem, s>>>(a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error("span kernel launch: %s", cudaGetErrorString(e));
-    return -2;
-  }
-  return 0;
-}
-
-template <typename P, typename F, bool PUSH, bool DEP>
-int run_span(const Call& c, cudaStream_t s) {
+int run_gather(const Call& c, cudaStream_t s) {
   auto a = make_params<P, F>(c);
-  // per-call node records (E, B, invvol widened to double), stream-ordered
   double* fn = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&fn, (size_t)a.NN * 8 * sizeof(double), s);
   if (e != cudaSuccess) {
@@ -107,37 +17,24 @@ int run_span(const Call& c, cudaStream_t s) {
     return -2;
   }
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
-  pack_nodes<F><<<pb, 256, 0, s>>>(PUSH ? a.E : nullptr, PUSH ? a.B : nullptr,
-                                   DEP ? a.invvol : nullptr, a.NN, fn);
+  pack_nodes<F, double><<<pb, 256, 0, s>>>(a.E, a.B, (const F*)nullptr, a.NN, fn);
   a.fnode = fn;
-  int rc;
-  if (DEP && is_pow2(c.scale))
-    rc = launch_span<P, F, PUSH, DEP, true>(a, c.count, s);
-  else
-    rc = launch_span<P, F, PUSH, DEP, false>(a, c.count, s);
+  const int grid = grid_for(gather_kernel<P, F>, 0, c.count, kThreads);
+  gather_kernel<P, F><<<grid, kThreads, 0, s>>>(a);
+  const int rc = launch_error("gather kernel launch");
   cudaFreeAsync(fn, s);
   return rc;
 }
 
 template <typename P, typename F>
-int run_gather(const Call& c, cudaStream_t s) {
-  auto a = make_params<P, F>(c);
-  const int grid = grid_for(gather_kernel<P, F>, 0, c.count);
-  gather_kernel<P, F><<<grid, kThreads, 0, s>>>(a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error("gather kernel launch: %s", cudaGetErrorString(e));
-    return -2;
-  }
-  return 0;
-}
-
-template <typename P, typename F>
 int dispatch(const Call& c, cudaStream_t s) {
+  typedef ParityPolicy<P, F> Pol;
+  // (base*m)*scale == (base*scale)*m exactly only for a power-of-two scale
+  const bool pre = is_pow2(c.scale);
   switch (c.op) {
-    case OP_FUSED: return run_span<P, F, true, true>(c, s);
-    case OP_PUSH: return run_span<P, F, true, false>(c, s);
-    case OP_DEPOSIT: return run_span<P, F, false, true>(c, s);
+    case OP_FUSED: return run_span<Pol, true, true>(c, pre, s);
+    case OP_PUSH: return run_span<Pol, true, false>(c, pre, s);
+    case OP_DEPOSIT: return run_span<Pol, false, true>(c, pre, s);
     case OP_GATHER: return run_gather<P, F>(c, s);
   }
   set_error("unknown op %d", c.op);

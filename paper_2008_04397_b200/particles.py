@@ -1,0 +1,248 @@
+"""Particle storage, batching, boundaries, sorting and loading on the path
+(reference ``pkg/src/batchpic/particles.py``).
+
+``ParticleBuffer`` is the reference's host SoA buffer (x y z u v w q_p +
+int64 ids).  ``DeviceParticles`` holds the same arrays as CUDA tensors —
+the layout the kernels stream — and converts to/from a host buffer.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .config import PrecisionMode
+from .errors import ConfigurationError, DomainError, IntegrityError
+from .geometry import PERIODIC
+
+COMPONENTS = ("x", "y", "z", "u", "v", "w")
+ARRAYS = COMPONENTS + ("q_p",)
+
+
+@dataclass
+class ParticleBuffer:
+    """One species in SoA layout (particles.py:23-81)."""
+
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+    q_p: np.ndarray
+    ids: np.ndarray
+    species_id: int = 0
+
+    @classmethod
+    def empty(cls, n, species_id=0, dtype=np.float64):
+        z = lambda: np.zeros(n, dtype=dtype)  # noqa: E731
+        return cls(x=z(), y=z(), z=z(), u=z(), v=z(), w=z(), q_p=z(),
+                   ids=np.arange(n, dtype=np.int64), species_id=species_id)
+
+    @property
+    def n(self):
+        return self.x.shape[0]
+
+    @property
+    def dtype(self):
+        return self.x.dtype
+
+    def components(self):
+        return tuple(getattr(self, c) for c in COMPONENTS)
+
+    def copy(self):
+        return ParticleBuffer(*(getattr(self, a).copy() for a in ARRAYS + ("ids",)),
+                              species_id=self.species_id)
+
+    def permute(self, order):
+        for a in ARRAYS + ("ids",):
+            setattr(self, a, np.ascontiguousarray(getattr(self, a)[order]))
+        return self
+
+    def validate(self, geom=None):
+        for a in ARRAYS + ("ids",):
+            if getattr(self, a).shape != (self.n,):
+                raise IntegrityError("particle component arrays disagree in length")
+        if geom is not None and self.n:
+            for q, o, L in zip((self.x, self.y, self.z), geom.origin, geom.lengths):
+                if q.min() < o or q.max() > o + L:
+                    raise IntegrityError("particle positions outside the domain")
+        return self
+
+
+@dataclass
+class BatchPlan:
+    spans: tuple
+    batches: int
+    group_of: tuple = field(default=())
+
+    def __post_init__(self):
+        if not self.group_of:
+            self.group_of = tuple(0 for _ in self.spans)
+
+
+def partition_batches(n_p, m):
+    """``m`` contiguous spans differing by at most one; the first
+    ``n_p % m`` take the extra particle (particles.py:97-114)."""
+    if m < 1:
+        raise ConfigurationError(f"batch count must be >= 1, got {m}")
+    if n_p < 0:
+        raise ConfigurationError(f"negative particle count {n_p}")
+    q, r = divmod(n_p, m)
+    spans, start = [], 0
+    for b in range(m):
+        ln = q + 1 if b < r else q
+        spans.append((start, ln))
+        start += ln
+    return BatchPlan(spans=tuple(spans), batches=m)
+
+
+def apply_boundaries(buf, geom):
+    """Vectorised boundary map with the kernel's exact branch semantics:
+    periodic wrap with snap-to-origin, reflecting mirror + velocity flip,
+    runaway -> IntegrityError (particles.py:117-154)."""
+    for pos, vel, o, L, kind in zip((buf.x, buf.y, buf.z), (buf.u, buf.v, buf.w),
+                                    geom.origin, geom.lengths, geom.bc):
+        if pos.size == 0:
+            continue
+        t = pos.dtype.type
+        Lc, oc = t(L), t(o)
+        hi = oc + Lc
+        if kind == PERIODIC:
+            below, above = pos < oc, pos >= hi
+            pos[below] += Lc
+            pos[below & (pos >= hi)] = oc
+            pos[above] -= Lc
+        else:
+            below, above = pos < oc, pos > hi
+            pos[below] = oc + (oc - pos[below])
+            vel[below] = -vel[below]
+            pos[above] = hi + hi - pos[above]
+            vel[above] = -vel[above]
+        if (pos < oc).any() or (pos > hi).any():
+            raise IntegrityError("particle left the domain by a full box length (runaway)")
+    return buf
+
+
+def sort_by_cell(buf, geom):
+    """Stable reorder by linear cell index (particles.py:157-167).  Host
+    buffers are sorted with numpy; use ``DeviceParticles.sort_by_cell`` for
+    device-resident particles."""
+    if buf.n == 0:
+        return buf
+    keys = geom.cell_index_of(buf.x, buf.y, buf.z)
+    return buf.permute(np.argsort(keys, kind="stable"))
+
+
+def cell_sequence(buf, geom):
+    if buf.n == 0:
+        return np.zeros(0, np.int64)
+    return geom.cell_index_of(buf.x, buf.y, buf.z)
+
+
+# --------------------------------------------------------------- loading
+
+def _species_rng(seed, species_id):
+    key = np.array([np.uint64(seed), np.uint64(species_id)], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def init_maxwellian(species, geom, density_fn=None, seed=1, precision=None, drift=None):
+    """Cell-major loading of ``ppc`` particles per cell, drifting Maxwellian
+    velocities, charge weights from the density at cell centres — the same
+    Philox(seed, species) draw sequence as particles.py:182-241, so buffers are
+    bit-identical to the reference's."""
+    mode = precision or PrecisionMode()
+    pd = mode.particle_dtype
+    ppc = species.ppc
+    nc = geom.n_cells
+    n_p = nc * ppc
+    rng = _species_rng(seed, species.species_id)
+    lin = np.arange(nc)
+    ci = lin % geom.nx
+    cj = (lin // geom.nx) % geom.ny
+    ck = lin // (geom.nx * geom.ny)
+    # positions are drawn before velocities
+    jit = rng.random((3, n_p))
+    pos = []
+    for a, cidx in enumerate((ci, cj, ck)):
+        d, o = geom.spacings[a], geom.origin[a]
+        corner = o + d * np.repeat(cidx, ppc)
+        pos.append(corner + d * jit[a])
+    dv = species.drift if drift is None else tuple(drift)
+    nrm = rng.standard_normal((3, n_p))
+    vel = [dv[a] + species.vth[a] * nrm[a] for a in range(3)]
+    if density_fn is None:
+        dens = np.ones(nc)
+    else:
+        cx, cy, cz = (geom.cell_centers(a) for a in range(3))
+        dens = np.asarray(density_fn(cx[ci], cy[cj], cz[ck]), dtype=np.float64)
+        if (dens <= 0.0).any():
+            raise ConfigurationError("density profile must be positive")
+    q_p = np.repeat(species.charge * dens * geom.cell_volume / ppc, ppc)
+    buf = ParticleBuffer(*(a.astype(pd) for a in pos + vel + [q_p]),
+                         ids=np.arange(n_p, dtype=np.int64), species_id=species.species_id)
+    return buf.validate(geom)
+
+
+# ------------------------------------------------------- device residency
+
+class DeviceParticles:
+    """One species' SoA arrays resident in HBM (CUDA torch tensors)."""
+
+    def __init__(self, x, y, z, u, v, w, q_p, ids, species_id=0):
+        self.x, self.y, self.z, self.u, self.v, self.w = x, y, z, u, v, w
+        self.q_p, self.ids, self.species_id = q_p, ids, species_id
+
+    @classmethod
+    def from_host(cls, buf, device, start=0, count=None):
+        import torch
+        count = buf.n - start if count is None else count
+        sl = slice(start, start + count)
+        t = [torch.from_numpy(np.ascontiguousarray(getattr(buf, a)[sl])).to(device)
+             for a in ARRAYS + ("ids",)]
+        return cls(*t, species_id=buf.species_id)
+
+    def to_host(self):
+        return ParticleBuffer(*(getattr(self, a).cpu().numpy() for a in ARRAYS + ("ids",)),
+                              species_id=self.species_id)
+
+    @property
+    def n(self):
+        return self.x.shape[0]
+
+    @property
+    def dtype(self):
+        return self.x.dtype
+
+    def arrays(self):
+        return tuple(getattr(self, a) for a in ARRAYS)
+
+    def nbytes(self):
+        return sum(getattr(self, a).numel() * getattr(self, a).element_size()
+                   for a in ARRAYS + ("ids",))
+
+    def sort_by_cell(self, geom, stream=None):
+        """On-device stable cell sort (bp_sort_by_cell): cell keys in f64 as
+        geometry.cell_index_of, stable radix sort, permutation of all eight
+        arrays in place."""
+        import torch
+        from . import _lib
+        if self.n <= 1:
+            return self
+        L = _lib.load()
+        o = np.ascontiguousarray(geom.origin, np.float64)
+        d = np.ascontiguousarray(geom.spacings, np.float64)
+        c = np.ascontiguousarray(geom.counts, np.int64)
+        s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        rc = L.bp_sort_by_cell(self.x.element_size(), *[ptr(a) for a in self.arrays()],
+                               ptr(self.ids), self.n, ctypes.c_void_p(o.ctypes.data),
+                               ctypes.c_void_p(d.ctypes.data), ctypes.c_void_p(c.ctypes.data),
+                               ctypes.c_void_p(s.cuda_stream))
+        _lib.check(rc, "sort_by_cell")
+        if rc == _lib.ERR_DOMAIN:
+            raise DomainError("positions below the box origin")
+        return self

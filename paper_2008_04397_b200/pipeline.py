@@ -1,0 +1,273 @@
+"""Device-resident cycle driver: phases 1-4 and 6 of the reference
+``pipeline.run_cycle`` (``pkg/src/batchpic/pipeline.py:228-324``) on B200s.
+
+  phase 1  E/B from the host solver -> HBM (rank 0), NCCL broadcast to ranks
+  phase 2  zero the per-species int64 accumulators
+  phase 3  fused mover + deposition per species over this rank's particle
+           shard (``bp_fused_span_ex``), optionally in batches; per-species
+           NCCL all-reduce (int64 sum, exact) issued as soon as the species'
+           kernels are queued so it overlaps the next species
+  phase 4  periodic fold of the moment grids on device, copy to the host
+  phase 6  on-device stable cell sort every ``sort_period`` cycles
+
+Particle decomposition (paper §III.A, re-targeted at GPUs): every species'
+particles are split into contiguous spans, one per rank (``shard_span``);
+every rank holds a full E/B copy and a full accumulator per species.  Integer
+moments make the result bit-identical for any rank count.
+
+The host field solve (phase 5) stays outside, as in the paper; a caller
+passes the new E/B in every cycle (``set_fields``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .config import PrecisionMode
+from .errors import ConfigurationError, IntegrityError
+from .fields import MOMENT_SCALE, N_MOMENTS
+from .particles import DeviceParticles, partition_batches
+
+
+def shard_span(n, rank, world):
+    """Contiguous span (start, count) of rank ``rank`` out of ``world`` for a
+    species of ``n`` particles (the reference's partition rule,
+    particles.py:97-114: the first n % world ranks take one extra)."""
+    return partition_batches(n, world).spans[rank]
+
+
+def reduce_moments(accs, group=None, async_op=False):
+    """Exact all-reduce (int64 SUM) of per-species moment grids across the
+    ranks of ``group`` (NCCL for CUDA tensors, gloo for CPU tensors).  Returns
+    the work handles when ``async_op``."""
+    import torch.distributed as dist
+    works = [dist.all_reduce(a, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+             for a in accs]
+    return works if async_op else None
+
+
+def broadcast_fields(E, B, src=0, group=None):
+    import torch.distributed as dist
+    dist.broadcast(E, src, group=group)
+    dist.broadcast(B, src, group=group)
+
+
+@dataclass
+class CycleTiming:
+    cycle: int
+    phase3_ms: float            # device time of phase 3 (kernels + reduce)
+    kernel_ms: float            # device time of the fused kernels alone
+    sort_ms: float = 0.0
+    particles: int = 0          # particles advanced by ALL ranks
+    sorted_this_cycle: bool = False
+
+    @property
+    def mpa_s(self):
+        return self.particles / (self.phase3_ms * 1e-3) / 1e6 if self.phase3_ms > 0 else 0.0
+
+
+@dataclass
+class DeviceSimulation:
+    """One rank's view of a device-resident simulation."""
+
+    geom: object
+    species: tuple
+    dt: float
+    c: float = 1.0
+    precision: PrecisionMode = field(default_factory=PrecisionMode)
+    arith: str = "parity"
+    sort_period: int = 10
+    batches: int = 1
+    device: object = None
+    group: object = None          # torch.distributed process group (None = default)
+    distributed: bool = False
+
+    def __post_init__(self):
+        import torch
+        self.torch = torch
+        if self.device is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        pd = torch.float32 if self.precision.particle_dtype == np.float32 else torch.float64
+        fd = torch.float32 if self.precision.field_dtype == np.float32 else torch.float64
+        self.pdt, self.fdt = pd, fd
+        shp = (3,) + self.geom.node_shape
+        self.E = torch.zeros(shp, dtype=fd, device=self.device)
+        self.B = torch.zeros(shp, dtype=fd, device=self.device)
+        self.invvol = torch.from_numpy(
+            self.geom.inv_node_volume(self.precision.field_dtype)).to(self.device)
+        self.acc = [torch.zeros((N_MOMENTS,) + self.geom.node_shape, dtype=torch.int64,
+                                device=self.device) for _ in self.species]
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.particles = [None] * len(self.species)
+        self.cycle = 0
+        from .kernels import make_geo_arrays, kernel_scalars
+        npd, nfd = self.precision.particle_dtype, self.precision.field_dtype
+        self.geo_f, self.geo_i = make_geo_arrays(self.geom, npd)
+        self.geo_g, _ = make_geo_arrays(self.geom, nfd)
+        self.geo_f = np.ascontiguousarray(self.geo_f, np.float64)
+        self.geo_g = np.ascontiguousarray(self.geo_g, np.float64)
+        self.scalars = [kernel_scalars(s, self.dt, self.c, npd) for s in self.species]
+        self.mixed = 1 if npd != nfd else 0
+        self.scale = float(nfd(MOMENT_SCALE))
+        self._arith = {"parity": _lib.ARITH_PARITY, "fast": _lib.ARITH_FAST}[self.arith]
+        if self.distributed:
+            import torch.distributed as dist
+            self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        else:
+            self.rank, self.world = 0, 1
+
+    # ------------------------------------------------------------ loading
+    def load_species(self, sid, parts):
+        """Install this rank's shard (a DeviceParticles) of species ``sid``."""
+        if parts.dtype != self.pdt:
+            raise ConfigurationError("particle dtype does not match the precision mode")
+        self.particles[sid] = parts
+
+    def load_host_buffers(self, buffers):
+        """Shard full host buffers (reference ParticleBuffers) onto this rank."""
+        for sid, buf in enumerate(buffers):
+            start, count = shard_span(buf.n, self.rank, self.world)
+            self.load_species(sid, DeviceParticles.from_host(buf, self.device, start, count))
+
+    def total_particles(self):
+        n = sum(p.n for p in self.particles if p is not None)
+        if self.distributed:
+            import torch.distributed as dist
+            t = self.torch.tensor([n], dtype=self.torch.int64, device=self.device)
+            dist.all_reduce(t, group=self.group)
+            n = int(t.item())
+        return n
+
+    # ------------------------------------------------------------ phases
+    def set_fields(self, E=None, B=None):
+        """Phase 1: host E/B (numpy, rank 0) -> HBM, broadcast to all ranks."""
+        if E is not None:
+            self.E.copy_(self.torch.from_numpy(np.ascontiguousarray(E)), non_blocking=False)
+        if B is not None:
+            self.B.copy_(self.torch.from_numpy(np.ascontiguousarray(B)), non_blocking=False)
+        if self.distributed:
+            broadcast_fields(self.E, self.B, src=0, group=self.group)
+
+    def _fused(self, sid, start, count, stream):
+        p = self.particles[sid]
+        sc = self.scalars[sid]
+        L = _lib.load()
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        hp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        rc = L.bp_fused_span_ex(
+            self._arith, p.x.element_size(), self.E.element_size(),
+            *[ptr(a) for a in p.arrays()], int(start), int(count), ptr(self.E), ptr(self.B),
+            ptr(self.acc[sid]), ptr(self.invvol), hp(self.geo_f), hp(self.geo_g),
+            hp(self.geo_i), float(sc["dt"]), float(sc["dth"]), float(sc["qdt2m"]),
+            float(sc["beta"]), float(sc["one"]), int(self.species[sid].mover_iters),
+            self.scale, self.mixed, ptr(self.status), ctypes.c_void_p(stream.cuda_stream))
+        _lib.check(rc, "fused_span")
+
+    def phase3(self, reduce=True):
+        """Phases 2-3 for every species; returns (phase3_ms, kernel_ms) of
+        device time on the compute stream (events), reduce included."""
+        torch = self.torch
+        s = torch.cuda.current_stream(self.device)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.status.zero_()
+        ev[0].record(s)
+        for a in self.acc:
+            a.zero_()
+        ev[1].record(s)
+        works = []
+        for sid, p in enumerate(self.particles):
+            if p is None or p.n == 0:
+                continue
+            for (b0, bn) in partition_batches(p.n, self.batches).spans:
+                if bn:
+                    self._fused(sid, b0, bn, s)
+            if reduce and self.distributed:
+                works += reduce_moments([self.acc[sid]], self.group, async_op=True)
+        ev[2].record(s)
+        for w in works:
+            w.wait()
+        ev[3].record(s)
+        ev[3].synchronize()
+        st = int(self.status.item())
+        if st == _lib.ERR_RUNAWAY:
+            raise IntegrityError("runaway particle (moved a full box length)")
+        if st == _lib.ERR_MIDPOINT:
+            raise IntegrityError("mover midpoint not mappable into the domain")
+        if st == _lib.ERR_DOMAIN:
+            raise IntegrityError("particle outside the domain at deposition")
+        return ev[0].elapsed_time(ev[3]), ev[1].elapsed_time(ev[2])
+
+    def fold_moments(self):
+        """Phase 4 on device: merge duplicated periodic planes (exact)."""
+        L = _lib.load()
+        gi = np.ascontiguousarray(self.geo_i, np.int64)
+        s = self.torch.cuda.current_stream(self.device)
+        for a in self.acc:
+            rc = L.bp_fold_periodic_i64(ctypes.c_void_p(a.data_ptr()), N_MOMENTS,
+                                        ctypes.c_void_p(gi.ctypes.data),
+                                        ctypes.c_void_p(s.cuda_stream))
+            _lib.check(rc, "fold_periodic")
+
+    def moments_host(self):
+        return [a.cpu().numpy() for a in self.acc]
+
+    def sort(self):
+        for p in self.particles:
+            if p is not None:
+                p.sort_by_cell(self.geom)
+
+    def run_cycle(self, E=None, B=None):
+        """One cycle on device: phases 1-4 and (when due) 6.  The host solve
+        (phase 5) is the caller's; moments for it are in ``self.acc``."""
+        torch = self.torch
+        if E is not None or B is not None:
+            self.set_fields(E, B)
+        p3, kt = self.phase3()
+        self.fold_moments()
+        sort_ms, sorted_now = 0.0, False
+        if self.sort_period > 0 and (self.cycle + 1) % self.sort_period == 0:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            self.sort()
+            e1.record()
+            e1.synchronize()
+            sort_ms, sorted_now = e0.elapsed_time(e1), True
+        t = CycleTiming(self.cycle, p3, kt, sort_ms, self.total_particles(), sorted_now)
+        self.cycle += 1
+        return t
+
+    # ------------------------------------------------------- diagnostics
+    def kinetic_energy(self):
+        """Per-species sum of (q_p / qom) |v|^2 / 2 in f64 over all ranks
+        (diagnostics.kinetic_energy, diagnostics.py:64-73)."""
+        torch = self.torch
+        out = []
+        for sp, p in zip(self.species, self.particles):
+            if p is None or p.n == 0:
+                k = torch.zeros((), dtype=torch.float64, device=self.device)
+            else:
+                u, v, w = (a.to(torch.float64) for a in (p.u, p.v, p.w))
+                m = p.q_p.to(torch.float64) / sp.qom
+                k = 0.5 * torch.sum(m * (u * u + v * v + w * w))
+            out.append(k)
+        t = torch.stack(out)
+        if self.distributed:
+            import torch.distributed as dist
+            dist.all_reduce(t, group=self.group)
+        return [float(x) for x in t.cpu()]
+
+
+def field_energy(E, B, geom):
+    """Sum of (|E|^2 + |B|^2) w V / 8 pi over unique nodes, f64
+    (diagnostics.field_energy, diagnostics.py:52-61)."""
+    sl = (slice(None),) + geom.unique_slices()
+    E = np.asarray(E, np.float64)[sl]
+    B = np.asarray(B, np.float64)[sl]
+    w = geom.node_weights()[geom.unique_slices()]
+    dens = (E * E).sum(axis=0) + (B * B).sum(axis=0)
+    return float(np.sum(dens * w)) * geom.cell_volume / (8.0 * np.pi)

@@ -2,7 +2,14 @@
 (128x64x64 cells, ppc 125 -> 65.5M particles), cell-sorted and shuffled."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import numpy as np, torch, threading
+try:
+    import pynvml; pynvml.nvmlInit(); _h = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:
+    _h = None
+def clocks():
+    if _h is None: return -1, -1
+    return pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM), pynvml.nvmlDeviceGetPowerUsage(_h) // 1000
 from paper_2008_04397_b200 import kernels as K
 from paper_2008_04397_b200.geometry import GridGeometry
 from paper_2008_04397_b200.config import SpeciesParams
@@ -54,8 +61,15 @@ for label in labels:
     it = int(os.environ.get("PROBE_IT", "5"))
     e0.record()
     for _ in range(it): run()
+    samples = []
+    stop = threading.Event()
+    def mon():
+        while not stop.is_set():
+            samples.append(clocks()); time.sleep(0.002)
+    th = threading.Thread(target=mon); th.start()
     e1.record(); torch.cuda.synchronize()
+    stop.set(); th.join()
     ms = e0.elapsed_time(e1) / it
     bytes_ = n * 13 * (4 if pd == torch.float32 else 8)
     print(f"{mode} {arith} {label}: n={n} {ms:.3f} ms/pass  {n/ms/1e6:.2f} G particles/s  "
-          f"{bytes_/ms/1e6:.0f} GB/s algorithmic  status={int(st.item())}", flush=True)
+          f"{bytes_/ms/1e6:.0f} GB/s algorithmic  status={int(st.item())} clk/W={samples[len(samples)//2] if samples else None}", flush=True)

@@ -158,3 +158,65 @@ def test_fused_empty_span_and_offsets(gpu, oracle):
         assert np.array_equal(r, t.cpu().numpy())
     with pytest.raises(IndexError):
         K.fused_span(*d, n - 10, 11, dE, dB, dacc, dinv, *tail)
+
+
+def _assert_close(name, ref, got, rtol, period=None):
+    ref = np.asarray(ref, np.float64)
+    got = np.asarray(got, np.float64)
+    d = np.abs(got - ref)
+    if period is not None:  # periodic axes: a wrap decided on the other side of the face
+        d = np.minimum(d, np.abs(period - d))
+    scale = max(np.abs(ref).max(), 1e-300)
+    worst = d.max() / scale if d.size else 0.0
+    assert worst <= rtol, f"{name}: max |diff| / max |ref| = {worst:.3e} > {rtol:.1e}"
+
+
+# north-star tolerances: 1e-10 (f64), 1e-4 (f32), relative to the array max
+FAST_RTOL = {"double": 1e-10, "single": 1e-4, "mixed": 1e-4}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("order", ["random", "sorted"])
+def test_fast_arith_within_tolerance_of_oracle(gpu, oracle, mode, order):
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 300_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(
+        mode, n, seed=17, order=order)
+    inv = geom.inv_node_volume(fd)
+    mixed = 1 if pd != fd else 0
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"],
+            sc["one"], 3, fd(SCALE), mixed)
+    ref = [a.copy() for a in arrs]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    st_ref = oracle.fused_span(*ref, 0, n, E, B, acc_ref, inv, *tail)
+    d = _dev(torch, arrs)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    st = K.fused_span(*d, 0, n, dE, dB, dacc, dinv, *tail, arith="fast")
+    assert st == st_ref
+    rtol = FAST_RTOL[mode]
+    periods = (geom.Lx, None, geom.Lz, None, None, None)
+    for name, r, t, per in zip("xyzuvw", ref, d, periods):
+        _assert_close(name, r, t.cpu().numpy(), rtol, per)
+    got = dacc.cpu().numpy()
+    for m in range(10):
+        _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, rtol)
+
+
+def test_fast_arith_deposit_is_order_independent(gpu):
+    """Fast arithmetic keeps the exact int64 lattice: a shuffled span deposits
+    bit-identical moments."""
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 200_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state("single", n, seed=5)
+    inv = geom.inv_node_volume(fd)
+    out = []
+    for perm in (np.arange(n), np.random.default_rng(1).permutation(n)):
+        d = _dev(torch, [a[perm] for a in arrs])
+        dinv = _dev(torch, [inv])[0]
+        dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+        K.deposit_span(*d, 0, n, dacc, dinv, geo_g, geo_i, fd(1.0), fd(SCALE))
+        out.append(dacc.cpu().numpy())
+    assert np.array_equal(out[0], out[1])
