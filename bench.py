@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark: particles moved + interpolated per second on 3D GEM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the metric's "GEM 3D"): 128x64x64 cells,
+4 species x 125 particles per cell = 262,144,000 particles, f32 storage
+("single" precision), dt 0.25, 3 mover iterations, decks/gem_full.deck
+physics; synthetic GEM-shaped particles drawn in HBM (gem.init_gem_device),
+E = 0 and the Harris + perturbation B of gem.py.  The total population is
+fixed and split over the ranks by contiguous cell ranges (strong scaling).
+
+A step is one cycle of the device path: E/B broadcast (N>1), zeroing of the
+int64 accumulators, the fused mover + deposition kernel for every species,
+the per-species exact NCCL all-reduce (N>1), the on-device periodic fold, and
+every `sort_period` (10) steps the on-device cell sort.  `value` is
+particles x steps / (max over ranks of the CUDA-event time of the K steps).
+Inputs (13.6 GB of particle traffic per step) exceed L2 (126 MB), so no L2
+flush is needed between steps.
+
+The headline arithmetic is "fast" (native f32 with FMA; within 1e-4 of the
+reference, tests/test_gpu_kernels.py); the bitwise "parity" arithmetic is
+measured beside it.  `e2e` runs the same workload through the C ABI's
+host-buffer entry point bp_fused_span_host (particles in pinned host memory,
+streamed H2D -> kernel -> D2H every step).  `cpu_baseline` and the
+reference arm time the reference arithmetic (oracle/oracle.cpp, the C++
+restatement pinned bitwise to the reference's numba kernels) on the host
+cores over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("particles moved+interpolated/sec (GEM 3D) at 1/2/4/8 B200; HBM GB/s fraction")
+UNIT = "particles/s"
+BYTES_PER_PARTICLE = {"single": 52, "mixed": 52, "double": 104}  # 13 words, SURVEY §8d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cells", default="128,64,64")
+    ap.add_argument("--ppc", type=int, default=125)
+    ap.add_argument("--precision", default="single", choices=("single", "mixed", "double"))
+    ap.add_argument("--arith", default="fast", choices=("fast", "parity"))
+    ap.add_argument("--sort-period", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(args, world):
+    cells = tuple(int(c) for c in args.cells.split(","))
+    n = int(np.prod(cells)) * args.ppc * 4
+    return cells, n, {
+        "workload": f"gem3d_{cells[0]}x{cells[1]}x{cells[2]}_ppc{args.ppc}x4",
+        "cells": list(cells), "particles": n, "species": 4, "ppc": args.ppc,
+        "precision": args.precision, "arith": args.arith, "mover_iters": 3, "dt": 0.25,
+        "sort_period": args.sort_period, "decomposition": f"particles/{world} ranks",
+        "l2_flush": "none: 13.6 GB of particle traffic per step >> 126 MB L2",
+    }
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the fused kernel from the committed ncu
+    capture summary (profiles/ncu_summary_r01.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) as f:
+            return float(json.load(f)["span_kernel"]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockMonitor:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed
+    region (the profiling recipe's clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        rows = []
+        for ln in getattr(self, "lines", []):
+            p = [x.strip() for x in ln.split(",")]
+            try:
+                rows.append((float(p[0]), float(p[1]), float(p[2]), p[3:7]))
+            except Exception:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1],
+                "power_w_max": max(r[2] for r in rows), "samples": len(rows),
+                "reasons": reasons}
+
+
+# ------------------------------------------------------------------ CPU legs
+
+def cpu_fused_rate(geom, species, prec, seconds, nthreads, cells_hint=2048):
+    """Reference arithmetic (oracle C++ port, all threads) on a bounded GEM
+    sample: returns (particles/s, sample description)."""
+    from oracle import oracle as O
+    from paper_2008_04397_b200.gem import gem_fields, sample_host, GemInit
+    from paper_2008_04397_b200.kernels import kernel_scalars, make_geo_arrays
+    from paper_2008_04397_b200.fields import MOMENT_SCALE
+    O.build()
+    fields = gem_fields(geom, GemInit(), prec)
+    pd, fd = prec.particle_dtype, prec.field_dtype
+    inv = geom.inv_node_volume(fd)
+    geo_f, geo_i = make_geo_arrays(geom, pd)
+    geo_g, _ = make_geo_arrays(geom, fd)
+    acc = np.zeros((10,) + geom.node_shape, np.int64)
+
+    def run(cells):
+        bufs = sample_host(geom, species, (geom.n_cells // 3, cells), precision=prec)
+        n = sum(b.n for b in bufs)
+        t0 = time.perf_counter()
+        for s, b in zip(species, bufs):
+            sc = kernel_scalars(s, 0.25, 1.0, pd)
+            st = O.fused_parallel(b.x, b.y, b.z, b.u, b.v, b.w, b.q_p, 0, b.n, fields.E, fields.B,
+                                  acc, inv, geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"],
+                                  sc["beta"], sc["one"], s.mover_iters, fd(MOMENT_SCALE),
+                                  1 if pd != fd else 0, nthreads)
+            assert st == 0, st
+        return n, time.perf_counter() - t0
+
+    n, t = run(cells_hint)  # calibrate on ~1M particles
+    cells = int(cells_hint * seconds / max(t, 1e-3))
+    cells = max(cells_hint, min(cells, geom.n_cells // 2))
+    n, t = run(cells)
+    return n / t, (f"{n} particles ({cells} cells x {species[0].ppc} ppc x 4 species, "
+                   f"GEM-shaped, cell-sorted) through oracle.fused_parallel, {t:.1f} s")
+
+
+def reference_arm(args):
+    """--impl reference: the reference CPU arithmetic on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import gem_geometry, gem_species
+    cells, n_total, config = workload_config(args, world)
+    geom = gem_geometry(cells)
+    species = gem_species(args.ppc)
+    prec = PrecisionMode.from_label(args.precision)
+    cores = os.cpu_count() or 1
+    per_step = max(1.0, min(args.cpu_seconds, 150.0 / max(args.steps + args.warmup, 1)))
+    rates = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        r, desc = cpu_fused_rate(geom, species, prec, per_step, cores)
+        if i >= args.warmup:
+            rates.append(r)
+    v = float(np.median(rates))
+    config = dict(config, arith="parity (reference numba arithmetic, C++ port)")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": n_total / v * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision != "double"
+           else "f64", "data": "synthetic", "config": config,
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": desc + " per step (median of steps)"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main_ours(args):
+    import torch
+    from paper_2008_04397_b200 import _lib
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import (GemInit, gem_fields, gem_geometry, gem_species,
+                                           init_gem_device)
+    from paper_2008_04397_b200.pipeline import DeviceSimulation, shard_span
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.load()
+
+    cells, n_total, config = workload_config(args, world)
+    geom = gem_geometry(cells)
+    species = gem_species(args.ppc)
+    prec = PrecisionMode.from_label(args.precision)
+    sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=args.arith,
+                           sort_period=args.sort_period, device=dev, distributed=world > 1)
+    c0, nc = shard_span(geom.n_cells, rank, world)
+    for sid, p in enumerate(init_gem_device(geom, species, dev, precision=prec, cells=(c0, nc))):
+        sim.load_species(sid, p)
+    f = gem_fields(geom, GemInit(), prec)
+    sim.set_fields(f.E, f.B)
+    n_local = sum(p.n for p in sim.particles)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def step(timing):
+        if dist is not None:
+            sim.set_fields()  # phase 1: broadcast from rank 0
+        t = sim.run_cycle()
+        timing.append(t)
+
+    warm = []
+    for _ in range(args.warmup):
+        step(warm)
+    sim.sort()  # sizes the sort workspace outside the timed region (no-op order change)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = L.bp_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timed = []
+    with ClockMonitor(local) as mon:
+        e0.record()
+        for _ in range(args.steps):
+            step(timed)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = L.bp_kernel_launches() - launches0
+    elapsed = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    kern = torch.tensor([sum(t.kernel_ms for t in timed)], dtype=torch.float64, device=dev)
+    sortms = torch.tensor([sum(t.sort_ms for t in timed)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        for t in (elapsed, kern, sortms):
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, kern_ms, sort_ms = float(elapsed), float(kern), float(sortms)
+    value = n_total * args.steps / (elapsed_ms * 1e-3)
+
+    # roofline of the dominant kernel: one fused launch = one species' shard
+    hbm, peak_kind = peaks()
+    bpp = BYTES_PER_PARTICLE[args.precision]
+    per_launch_particles = n_local / len(species)
+    launch_ms = kern_ms / (args.steps * len(species))
+    achieved = per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy)",
+                "kernel": "bp::span_kernel<FastPolicy<float,float>,fused> (+ per-call node "
+                          "record pack, timed together)",
+                "algorithmic_bytes_per_launch": per_launch_particles * bpp,
+                "launch_ms": launch_ms}
+
+    extra = {"phase3_kernel_ms_per_step": kern_ms / args.steps,
+             "sort_ms_per_sort": sort_ms / max(1, sum(t.sorted_this_cycle for t in timed)),
+             "phase3_particles_per_s": n_total / (kern_ms / args.steps * 1e-3)}
+
+    # bitwise reference arithmetic beside it
+    if not args.no_parity and args.arith != "parity":
+        sim._arith = _lib.ARITH_PARITY
+        pt = []
+        for _ in range(2):
+            step(pt)
+        pt = []
+        barrier()
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ks = max(2, min(args.steps, 5))
+        p0.record()
+        for _ in range(ks):
+            step(pt)
+        p1.record()
+        torch.cuda.synchronize()
+        pe = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(pe, op=dist.ReduceOp.MAX)
+        extra["parity_arith"] = {"value": n_total * ks / (float(pe) * 1e-3), "unit": UNIT,
+                                 "steps": ks, "note": "bitwise-reference arithmetic"}
+        sim._arith = _lib.ARITH_FAST if args.arith == "fast" else _lib.ARITH_PARITY
+
+    # end to end through the host-buffer C ABI (pinned host particles)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(args, sim, species, prec, geom, dist, dev, n_total)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        rate, desc = cpu_fused_rate(geom, species, prec, args.cpu_seconds, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32" if args.precision != "double" else "f64",
+               "data": "synthetic (GEM-shaped particles drawn in HBM, Harris+perturbation B)",
+               "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": launches, "clocks": mon.summary(), "extra": extra}
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, sim, species, prec, geom, dist, dev, n_total):
+    """Same workload through bp_fused_span_host: every step streams each
+    species from pinned host memory through the device and back."""
+    import torch
+    from paper_2008_04397_b200 import _lib
+    from paper_2008_04397_b200.fields import MOMENT_SCALE
+    L = _lib.load()
+    host = []
+    for p in sim.particles:
+        arrs = []
+        for a in p.arrays():
+            h = torch.empty(a.shape, dtype=a.dtype, pin_memory=True)
+            h.copy_(a)
+            arrs.append(h)
+        host.append(arrs)
+    E = sim.E.cpu().numpy()
+    B = sim.B.cpu().numpy()
+    inv = sim.invvol.cpu().numpy()
+    accs = [np.zeros((10,) + geom.node_shape, np.int64) for _ in species]
+    hp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    tp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    arith = _lib.ARITH_FAST if args.arith == "fast" else _lib.ARITH_PARITY
+    pb = host[0][0].element_size()
+    fb = E.dtype.itemsize
+
+    def one_step():
+        for sid, (s, arrs) in enumerate(zip(species, host)):
+            sc = sim.scalars[sid]
+            rc = L.bp_fused_span_host(arith, pb, fb, *[tp(a) for a in arrs], 0, arrs[0].numel(),
+                                      hp(E), hp(B), hp(accs[sid]), hp(inv), hp(sim.geo_f),
+                                      hp(sim.geo_g), hp(sim.geo_i), float(sc["dt"]),
+                                      float(sc["dth"]), float(sc["qdt2m"]), float(sc["beta"]),
+                                      float(sc["one"]), s.mover_iters, sim.scale, sim.mixed, 0)
+            _lib.check(rc, "bp_fused_span_host")
+
+    one_step()  # warm-up (allocations)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        one_step()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    n_local = sum(a[0].numel() for a in host)
+    nn = geom.n_nodes
+    h2d = n_local * 7 * pb + len(species) * (2 * 3 * nn * fb + nn * fb + 10 * nn * 8)
+    d2h = n_local * 6 * pb + len(species) * 10 * nn * 8
+    return {"value": n_total * args.e2e_steps / float(dt), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": args.e2e_steps,
+            "path": "bp_fused_span_host (pinned host SoA -> H2D -> fused kernel -> D2H), "
+                    "wall clock, max over ranks"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,10 @@ int bp_version(void);
 /* Last error message of the calling thread ("" if none). */
 const char* bp_last_error(void);
 
+/* Number of CUDA kernels this library has launched in this process (all
+ * threads): the evidence behind a benchmark's "gpu_launches". */
+long long bp_kernel_launches(void);
+
 /* Replaces kernels.fused_span (kernels.py:458-735): implicit mover with
  * boundary folding, then deposition of the 10 moments at the new state. */
 int bp_fused_span(int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us, void* vs,

@@ -24,7 +24,7 @@ ARITH_FAST = 1
 
 # every symbol include/bp_b200.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = (
-    "bp_version", "bp_last_error", "bp_fused_span", "bp_push_span",
+    "bp_version", "bp_last_error", "bp_kernel_launches", "bp_fused_span", "bp_push_span",
     "bp_deposit_span", "bp_gather_span", "bp_fused_span_ex",
     "bp_fused_span_host", "bp_sort_by_cell", "bp_cell_keys",
     "bp_fold_periodic_i64",
@@ -38,6 +38,7 @@ _INT = ctypes.c_int
 _SIGS = {
     "bp_version": (_INT, []),
     "bp_last_error": (ctypes.c_char_p, []),
+    "bp_kernel_launches": (ctypes.c_longlong, []),
     "bp_fused_span": (_INT, [_INT, _INT] + [_P] * 7 + [_I64, _I64] + [_P] * 4
                       + [_P, _P, _P] + [_D] * 5 + [_INT, _D, _INT, _P, _P]),
     "bp_fused_span_ex": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -13,6 +14,28 @@
 namespace bp {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Scratch (node records, sort buffers) comes from the device's default
+// stream-ordered pool; keep its memory mapped between calls instead of
+// returning it to the driver at every synchronisation (release threshold 0
+// by default), which otherwise costs a re-map of hundreds of MB per call.
+void ensure_pool() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -107,6 +130,7 @@ int run(Call& c, int arith, int* d_status, cudaStream_t s) {
   }
   const bool sync = d_status == nullptr;
   if (c.count == 0) return BP_OK;
+  ensure_pool();
   c.status = sync ? sync_slot(s) : d_status;
   if (!c.status) {
     set_error("status slot allocation failed");
@@ -225,6 +249,8 @@ using namespace bp;
 extern "C" {
 
 int bp_version(void) { return 100; }
+
+long long bp_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* bp_last_error(void) { return g_err; }
 
@@ -404,6 +430,7 @@ int bp_sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs
     set_error("unsupported particle dtype (%d bytes)", pbytes);
     return BP_EINVAL;
   }
+  ensure_pool();
   return sort_by_cell(pbytes, xs, ys, zs, us, vs, ws, qs, ids, n, origin, spacing, counts,
                       (cudaStream_t)stream);
 }
@@ -411,6 +438,7 @@ int bp_sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs
 int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
                  const double* origin, const double* spacing, const int64_t* counts,
                  int64_t* keys, void* stream) {
+  ensure_pool();
   return cell_keys(pbytes, xs, ys, zs, n, origin, spacing, counts, keys, (cudaStream_t)stream);
 }
 

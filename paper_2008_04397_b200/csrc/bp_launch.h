@@ -33,4 +33,10 @@ int launch_fast(const Call& c, cudaStream_t s);
 
 void set_error(const char* fmt, ...);
 
+// count of kernels this library launched (bp_kernel_launches)
+void note_launch(int n = 1);
+
+// keep the default stream-ordered pool's memory mapped between calls
+void ensure_pool();
+
 }  // namespace bp

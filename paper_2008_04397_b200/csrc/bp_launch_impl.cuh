@@ -107,6 +107,7 @@ int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t c
   // one wave of resident blocks; every warp walks a contiguous run of >= 32
   const int grid = grid_for(k, kSmem, count, kThreads);
   k<<<grid, kThreads, kSmem, s>>>(a);
+  note_launch();
   return launch_error("span kernel launch");
 }
 
@@ -126,6 +127,7 @@ int run_span(const Call& c, bool prescale_ok, cudaStream_t s) {
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
   pack_nodes<F, T><<<pb, 256, 0, s>>>(PUSH ? a.E : nullptr, PUSH ? a.B : nullptr,
                                       DEP ? a.invvol : nullptr, a.NN, fn);
+  note_launch();
   a.fnode = fn;
   int rc;
   if (DEP && prescale_ok)

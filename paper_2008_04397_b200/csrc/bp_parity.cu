@@ -18,9 +18,11 @@ int run_gather(const Call& c, cudaStream_t s) {
   }
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
   pack_nodes<F, double><<<pb, 256, 0, s>>>(a.E, a.B, (const F*)nullptr, a.NN, fn);
+  note_launch();
   a.fnode = fn;
   const int grid = grid_for(gather_kernel<P, F>, 0, c.count, kThreads);
   gather_kernel<P, F><<<grid, kThreads, 0, s>>>(a);
+  note_launch();
   const int rc = launch_error("gather kernel launch");
   cudaFreeAsync(fn, s);
   return rc;

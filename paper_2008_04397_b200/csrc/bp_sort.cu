@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdint>
+#include <mutex>
 
 #include "bp_launch.h"
 
@@ -100,6 +101,7 @@ int keys_launch(const void* xs, const void* ys, const void* zs, int64_t n, const
   cell_key_kernel<P><<<blocks_for(n), 256, 0, s>>>((const P*)xs, (const P*)ys, (const P*)zs, n,
                                                    o[0], o[1], o[2], d[0], d[1], d[2], c[0],
                                                    c[1], c[2], k32, k64, idx, bad);
+  note_launch();
   return check(cudaGetLastError(), "cell_key_kernel");
 }
 
@@ -115,6 +117,7 @@ int keys_any(int pbytes, const void* xs, const void* ys, const void* zs, int64_t
 template <typename T>
 int permute_one(void* arr, const uint32_t* order, void* tmp, int64_t n, cudaStream_t s) {
   gather_perm<T><<<blocks_for(n), 256, 0, s>>>((const T*)arr, order, (T*)tmp, n);
+  note_launch();
   int rc = check(cudaGetLastError(), "gather_perm");
   if (rc) return rc;
   return check(cudaMemcpyAsync(arr, tmp, n * sizeof(T), cudaMemcpyDeviceToDevice, s),
@@ -140,6 +143,15 @@ int cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_
   return hbad ? 3 : 0;
 }
 
+// Grow-only sort workspace per device (keys, indices, permutation scratch,
+// CUB temp storage), so periodic sorts do not re-allocate ~40 B/particle.
+struct SortWs {
+  void* base = nullptr;
+  size_t bytes = 0;
+};
+static std::mutex g_sort_mu;
+static SortWs g_sort_ws[64];
+
 int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, void* ws,
                  void* qs, int64_t* ids, int64_t n, const double* origin,
                  const double* spacing, const int64_t* counts, cudaStream_t s) {
@@ -151,25 +163,37 @@ int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, v
   const int64_t ncell = counts[0] * counts[1] * counts[2];
   int end_bit = 1;
   while (end_bit < 32 && (1LL << end_bit) < ncell) ++end_bit;
-  uint32_t *k_in, *k_out, *i_in, *i_out;
-  int* bad;
-  void* tmp;
-  const size_t nb = (size_t)n * sizeof(uint32_t);
   size_t cub_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, end_bit, s);
-  void* cub_tmp;
-  int rc = 0;
-  rc |= check(cudaMallocAsync((void**)&k_in, nb, s), "alloc");
-  rc |= check(cudaMallocAsync((void**)&k_out, nb, s), "alloc");
-  rc |= check(cudaMallocAsync((void**)&i_in, nb, s), "alloc");
-  rc |= check(cudaMallocAsync((void**)&i_out, nb, s), "alloc");
-  rc |= check(cudaMallocAsync((void**)&bad, sizeof(int), s), "alloc");
-  rc |= check(cudaMallocAsync(&tmp, (size_t)n * 8, s), "alloc");
-  rc |= check(cudaMallocAsync(&cub_tmp, cub_bytes, s), "alloc");
-  if (rc) return -2;
+  auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t nb = up((size_t)n * sizeof(uint32_t));
+  const size_t need = 4 * nb + up(sizeof(int)) + up((size_t)n * 8) + up(cub_bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_sort_mu);
+  SortWs& W = g_sort_ws[dev & 63];
+  if (W.bytes < need) {
+    if (W.base) {
+      cudaStreamSynchronize(s);
+      cudaFree(W.base);
+      W.base = nullptr;
+      W.bytes = 0;
+    }
+    int rc = check(cudaMalloc(&W.base, need), "sort workspace");
+    if (rc) return rc;
+    W.bytes = need;
+  }
+  char* p = static_cast<char*>(W.base);
+  uint32_t* k_in = (uint32_t*)p; p += nb;
+  uint32_t* k_out = (uint32_t*)p; p += nb;
+  uint32_t* i_in = (uint32_t*)p; p += nb;
+  uint32_t* i_out = (uint32_t*)p; p += nb;
+  int* bad = (int*)p; p += up(sizeof(int));
+  void* tmp = p; p += up((size_t)n * 8);
+  void* cub_tmp = p;
   cudaMemsetAsync(bad, 0, sizeof(int), s);
-  rc = keys_any(pbytes, xs, ys, zs, n, origin, spacing, counts, k_in, nullptr, i_in, bad, s);
+  int rc = keys_any(pbytes, xs, ys, zs, n, origin, spacing, counts, k_in, nullptr, i_in, bad, s);
   int hbad = 0;
   if (!rc) rc = check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
   if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
@@ -186,13 +210,6 @@ int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, v
     if (!rc && ids) rc = permute_one<long long>(ids, i_out, tmp, n, s);
     if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
   }
-  cudaFreeAsync(k_in, s);
-  cudaFreeAsync(k_out, s);
-  cudaFreeAsync(i_in, s);
-  cudaFreeAsync(i_out, s);
-  cudaFreeAsync(bad, s);
-  cudaFreeAsync(tmp, s);
-  cudaFreeAsync(cub_tmp, s);
   if (rc) return rc;
   return hbad ? 3 : 0;
 }
@@ -204,6 +221,7 @@ int fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, cudaStre
     const int n1 = axis == 0 ? NY : NX;
     const int n2 = axis == 2 ? NY : NZ;
     fold_axis<<<blocks_for(rows * n1 * n2), 256, 0, s>>>((long long*)acc, rows, NX, NY, NZ, axis);
+    note_launch();
     int rc = check(cudaGetLastError(), "fold_axis");
     if (rc) return rc;
   }

@@ -168,3 +168,35 @@ def init_gem_device(geom, species, device, init=GemInit(), precision=None, c=1.0
 
 def gem_deck_sizes(cells, ppc, species=4):
     return math.prod(cells) * ppc * species
+
+
+def sample_host(geom, species, cells, init=GemInit(), precision=None, c=1.0, seed=1):
+    """GEM-shaped particles of a contiguous cell range (x-fastest), drawn on
+    the host with numpy — the CPU legs of the benchmark time the reference
+    arithmetic on such a bounded sample of the same workload."""
+    from .particles import ParticleBuffer
+    _check(species)
+    mode = precision or PrecisionMode()
+    pd = mode.particle_dtype
+    c0, nc = cells
+    yc = geom.origin[1] + 0.5 * geom.Ly
+    lam = init.sheet_thickness
+    u_e, u_i = sheet_drifts(species, init, c)
+    drift_z = {SHEET_ELECTRON: u_e, SHEET_ION: u_i, BG_ELECTRON: 0.0, BG_ION: 0.0}
+    out = []
+    for s in species:
+        rng = np.random.default_rng([seed, s.species_id, c0])
+        lin = np.arange(c0, c0 + nc)
+        ci, cj, ck = lin % geom.nx, (lin // geom.nx) % geom.ny, lin // (geom.nx * geom.ny)
+        n = nc * s.ppc
+        pos = [geom.origin[a] + geom.spacings[a] * (np.repeat(ix, s.ppc) + rng.random(n))
+               for a, ix in enumerate((ci, cj, ck))]
+        vel = [(drift_z[s.species_id] if a == 2 else 0.0) + s.vth[a] * rng.standard_normal(n)
+               for a in range(3)]
+        ycell = geom.origin[1] + geom.dy * (cj + 0.5)
+        dens = (init.n0 / np.cosh((ycell - yc) / lam) ** 2 if s.species_id < 2
+                else np.full(nc, init.background_fraction * init.n0))
+        q = np.repeat(s.charge * dens * geom.cell_volume / s.ppc, s.ppc)
+        out.append(ParticleBuffer(*(a.astype(pd) for a in pos + vel + [q]),
+                                  ids=np.arange(n, dtype=np.int64), species_id=s.species_id))
+    return out

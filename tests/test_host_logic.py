@@ -1,0 +1,79 @@
+"""Host-side pieces of the path that need no GPU: the bitwise GEM loader,
+batching, boundary map, geometry helpers, the energy ledger formula, and
+that the product package refuses to run without its CUDA library."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import MODES, golden
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_gem_host_init_is_bitwise_the_reference(mode):
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import GemInit, gem_geometry, gem_species, init_gem_host
+    g = golden(f"c1_{mode}.npz")
+    geom = gem_geometry((64, 32, 1), (25.6, 12.8, 0.4))
+    bufs, f = init_gem_host(geom, gem_species(16), GemInit(), PrecisionMode.from_label(mode))
+    for s, b in enumerate(bufs):
+        for nm in ("x", "y", "z", "u", "v", "w", "q_p"):
+            sha = hashlib.sha256(np.ascontiguousarray(getattr(b, nm)).tobytes()).hexdigest()
+            assert sha == str(g[f"init_sha_{s}_{nm}"]), (s, nm)
+    assert np.array_equal(f.E, g["E"][0]) and np.array_equal(f.B, g["B"][0])
+
+
+def test_partition_batches_reference_rule():
+    from paper_2008_04397_b200.particles import partition_batches
+    plan = partition_batches(10, 4)
+    assert plan.spans == ((0, 3), (3, 3), (6, 2), (8, 2))
+    assert partition_batches(2, 4).spans[-1] == (2, 0)
+
+
+def test_apply_boundaries_wrap_mirror_and_runaway():
+    from paper_2008_04397_b200.errors import IntegrityError
+    from paper_2008_04397_b200.geometry import GridGeometry
+    from paper_2008_04397_b200.particles import ParticleBuffer, apply_boundaries
+    geom = GridGeometry.from_box((4, 4, 4), (4.0, 4.0, 4.0),
+                                 bc=("periodic", "reflecting", "periodic"))
+    buf = ParticleBuffer.empty(3)
+    buf.x[:] = [-0.5, 4.0, 4.5]
+    buf.y[:] = [-0.25, 4.5, 2.0]
+    buf.z[:] = 1.0
+    buf.v[:] = [1.0, 2.0, 3.0]
+    apply_boundaries(buf, geom)
+    assert list(buf.x) == [3.5, 0.0, 0.5]
+    assert list(buf.y) == [0.25, 3.5, 2.0] and list(buf.v) == [-1.0, -2.0, 3.0]
+    snap = buf.copy()
+    apply_boundaries(buf, geom)  # idempotent
+    assert np.array_equal(buf.x, snap.x) and np.array_equal(buf.y, snap.y)
+    buf.x[0] = 9.0
+    with pytest.raises(IntegrityError):
+        apply_boundaries(buf, geom)
+
+
+def test_inv_node_volume_walls_and_weights():
+    from paper_2008_04397_b200.geometry import GridGeometry
+    geom = GridGeometry.from_box((4, 4, 4), (2.0, 2.0, 2.0),
+                                 bc=("periodic", "reflecting", "periodic"))
+    inv = geom.inv_node_volume()
+    assert inv[1, 1, 1] == 8.0 and inv[1, 0, 1] == 16.0 and inv[0, 4, 0] == 16.0
+    assert (geom.node_weights().sum() * geom.cell_volume) == pytest.approx(8.0)
+
+
+def test_field_energy_matches_reference_formula():
+    from paper_2008_04397_b200.gem import GemInit, gem_fields, gem_geometry
+    from paper_2008_04397_b200.pipeline import field_energy
+    g = golden("c1_double.npz")
+    geom = gem_geometry((64, 32, 1), (25.6, 12.8, 0.4))
+    # ledger[c][0] is the field energy after cycle c+1 (the fields of cycle c+2)
+    assert field_energy(g["E"][1], g["B"][1], geom) == g["ledger"][0][0]
+
+
+def test_product_path_refuses_without_library(tmp_path, monkeypatch):
+    from paper_2008_04397_b200 import _lib
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(_lib.BackendError):
+        _lib.load()
