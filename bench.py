@@ -178,10 +178,11 @@ def cpu_fused_rate(geom, species, prec, seconds, nthreads, cells_hint=2048):
             assert st == 0, st
         return n, time.perf_counter() - t0
 
-    n, t = run(cells_hint)  # calibrate on ~1M particles
-    cells = int(cells_hint * seconds / max(t, 1e-3))
-    cells = max(cells_hint, min(cells, geom.n_cells // 2))
-    n, t = run(cells)
+    cells = cells_hint
+    n, t = run(cells)  # grow the sample until it is ~`seconds` of CPU work
+    while t < 0.5 * seconds and cells < geom.n_cells // 2:
+        cells = min(geom.n_cells // 2, int(cells * min(8.0, max(2.0, seconds / max(t, 1e-3)))))
+        n, t = run(cells)
     return n / t, (f"{n} particles ({cells} cells x {species[0].ppc} ppc x 4 species, "
                    f"GEM-shaped, cell-sorted) through oracle.fused_parallel, {t:.1f} s")
 

@@ -118,12 +118,17 @@ __device__ __forceinline__ void red_add(i64* p, i64 v) {
   if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
-// shared-memory staging of one warp (doubles): bases [32][8] and moments
-// [32][4][4] laid out so lane group g reads (m_g, m_g+4) with one 16-byte
-// load and m_g+8 (zero for g >= 2) with a second
-constexpr int kStageBs = 32 * 8;
-constexpr int kStageMv = 32 * 16;
-constexpr int kWarpStage = kStageBs + kStageMv + 16;  // + 32 int keys
+// Shared-memory staging of one warp (doubles), particle-minor so a lane reads
+// the values of two consecutive particles with one 16-byte load:
+//   bases   [corner c][particle]            8 rows
+//   moments [group g][slot j][particle]     12 rows: slot j of group g holds
+//           moment g + 4j (zero for g + 4j >= 10)
+// Rows are padded to 34 doubles (272 B) so the 8 corner rows / 4 group rows
+// read by one warp instruction fall in distinct banks.
+constexpr int kRow = 34;
+constexpr int kStageBs = 8 * kRow;
+constexpr int kStageMv = 12 * kRow;
+constexpr int kWarpStage = kStageBs + kStageMv;
 
 // Exact rint without the conversion pipe: for |t| < 2^51, t + 1.5*2^52 lands
 // in [2^52, 2^53) where the ulp is 1, so the FP add rounds t half-to-even
@@ -165,59 +170,52 @@ __device__ __forceinline__ u64 qbits(double b, double m, double sc) {
   return (u64)__double2ll_rn(t) + (u64)kMagicBits;
 }
 
-template <bool PRESCALE, bool MAGIC, bool FMA>
-__device__ __forceinline__ void fold_vals(u64& s0, u64& s1, u64& s2, const double* st_bs,
-                                          const double* st_mv, int k, int lc, int lg,
-                                          double sc) {
-  const double b = st_bs[k * 8 + lc];
-  const double2 m01 = *reinterpret_cast<const double2*>(st_mv + k * 16 + lg * 4);
-  const double m2 = st_mv[k * 16 + lg * 4 + 2];
-  s0 += qbits<PRESCALE, MAGIC, FMA>(b, m01.x, sc);
-  s1 += qbits<PRESCALE, MAGIC, FMA>(b, m01.y, sc);
-  s2 += qbits<PRESCALE, MAGIC, FMA>(b, m2, sc);  // m2 == 0 for lane groups 2, 3
-}
-
+// staged particle k into S: this lane's corner lc of moments lg, lg+4, lg+8
 template <bool PRESCALE, bool MAGIC, bool FMA>
 __device__ __forceinline__ void fold_one(Slot& S, const double* st_bs, const double* st_mv,
                                          int k, int lc, int lg, double sc) {
-  fold_vals<PRESCALE, MAGIC, FMA>(S.s0, S.s1, S.s2, st_bs, st_mv, k, lc, lg, sc);
+  const double b = st_bs[lc * kRow + k];
+  const double* mv = st_mv + lg * 3 * kRow + k;
+  S.s0 += qbits<PRESCALE, MAGIC, FMA>(b, mv[0], sc);
+  S.s1 += qbits<PRESCALE, MAGIC, FMA>(b, mv[kRow], sc);
+  S.s2 += qbits<PRESCALE, MAGIC, FMA>(b, mv[2 * kRow], sc);  // 0 for lane groups 2, 3
   S.n += 1;
 }
 
-// all 32 staged particles into S, two interleaved chains
+// All 32 staged particles into S, two particles per step: one 16-byte load
+// per staged row, and the two contributions of a value summed with one
+// 3-input 64-bit add (IADD3 + IADD3.X).
 template <bool PRESCALE, bool MAGIC, bool FMA>
 __device__ __forceinline__ void fold_tile(Slot& S, const double* st_bs, const double* st_mv,
                                           int lc, int lg, double sc) {
-  u64 t0 = 0, t1 = 0, t2 = 0;
-#pragma unroll 8
+  const double* br = st_bs + lc * kRow;
+  const double* mr = st_mv + lg * 3 * kRow;
+#pragma unroll 4
   for (int k = 0; k < 32; k += 2) {
-    fold_vals<PRESCALE, MAGIC, FMA>(S.s0, S.s1, S.s2, st_bs, st_mv, k, lc, lg, sc);
-    fold_vals<PRESCALE, MAGIC, FMA>(t0, t1, t2, st_bs, st_mv, k + 1, lc, lg, sc);
+    const double2 b = *reinterpret_cast<const double2*>(br + k);
+    const double2 m0 = *reinterpret_cast<const double2*>(mr + k);
+    const double2 m1 = *reinterpret_cast<const double2*>(mr + kRow + k);
+    const double2 m2 = *reinterpret_cast<const double2*>(mr + 2 * kRow + k);
+    S.s0 += qbits<PRESCALE, MAGIC, FMA>(b.x, m0.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m0.y, sc);
+    S.s1 += qbits<PRESCALE, MAGIC, FMA>(b.x, m1.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m1.y, sc);
+    S.s2 += qbits<PRESCALE, MAGIC, FMA>(b.x, m2.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m2.y, sc);
   }
-  S.s0 += t0; S.s1 += t1; S.s2 += t2;
   S.n += 32;
 }
 
-// Stage the moment values m0..m9 = 1 u v w uu uv uw vv vw ww of one particle,
-// grouped (g, g+4, g+8) per lane group.
+// Stage the moment values m0..m9 = 1 u v w uu uv uw vv vw ww of one particle
+// into its column (mv = st_mv + lane): row g*3 + j holds moment g + 4j.
 __device__ __forceinline__ void stage_moments(double* mv, double u, double v, double w,
                                               double uu, double uv, double uw, double vv,
                                               double vw, double ww) {
-  double2* m2 = reinterpret_cast<double2*>(mv);
-  m2[0] = make_double2(1.0, uu);
-  m2[1] = make_double2(vw, 0.0);
-  m2[2] = make_double2(u, uv);
-  m2[3] = make_double2(ww, 0.0);
-  m2[4] = make_double2(v, uw);
-  m2[5] = make_double2(0.0, 0.0);
-  m2[6] = make_double2(w, vv);
-  m2[7] = make_double2(0.0, 0.0);
+  const double r[12] = {1.0, uu, vw, u, uv, ww, v, uw, 0.0, w, vv, 0.0};
+#pragma unroll
+  for (int i = 0; i < 12; ++i) mv[i * kRow] = r[i];
 }
 
 __device__ __forceinline__ void stage_bases(double* st, const double bs[8]) {
-  double2* b2 = reinterpret_cast<double2*>(st);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) b2[c] = make_double2(bs[2 * c], bs[2 * c + 1]);
+  for (int c = 0; c < 8; ++c) st[c * kRow] = bs[c];
 }
 
 // |value| < 2^50 for every (corner, moment) keeps the magic rint exact
@@ -260,6 +258,25 @@ __device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict_
       A.s0 = A.s1 = A.s2 = 0;
     }
     MA = __ballot_sync(0xffffffffu, has && key == A.key);
+  } else if (MA != V) {
+    // a sorted run crossing into its next cell: once the new cell holds
+    // the majority of the tile, make it the main slot
+    const int kc = __shfl_sync(0xffffffffu, key, 31 - __clz(V));
+    const unsigned MC = __ballot_sync(0xffffffffu, has && key == kc);
+    if (__popc(MC) > __popc(MA)) {
+      if (kc == Bs.key) {
+        const Slot t = A;
+        A = Bs;
+        Bs = t;
+      } else {
+        slot_flush(Bs, acc, NN, lg, coff, third);
+        Bs = A;
+        A.key = kc;
+        A.n = 0;
+        A.s0 = A.s1 = A.s2 = 0;
+      }
+      MA = MC;
+    }
   }
   const unsigned strays = V & ~MA;
   unsigned rest = strays;
@@ -283,9 +300,8 @@ __device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict_
   }
   if (strays) {
     if ((strays >> lane) & 1u) {
-      double2* b2 = reinterpret_cast<double2*>(st_bs + lane * 8);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) b2[c] = make_double2(0.0, 0.0);
+      for (int c = 0; c < 8; ++c) st_bs[c * kRow + lane] = 0.0;
     }
     __syncwarp();
   }
@@ -351,7 +367,7 @@ __global__ void __launch_bounds__(256, 2)
     if (DO_DEPOSIT) {
       bool big = false;
       const int key = Pol::template stage<PRESCALE>(a, valid, xp, yp, zp, un, vn, wn, qp,
-                                                    st_bs + lane * 8, st_mv + lane * 16, big);
+                                                    st_bs + lane, st_mv + lane, big);
       if (valid && key < 0) worst = ST_DOMAIN > worst ? ST_DOMAIN : worst;
       __syncwarp();
       deposit_tile<PRESCALE, Pol::kFmaFold>(A, Bs, a.acc, a.NN, key, big, st_bs, st_mv, lane,
