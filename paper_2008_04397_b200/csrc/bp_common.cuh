@@ -66,6 +66,9 @@ struct SpanParams {
   // per-call node records (pack_nodes), element type Policy::NodeT:
   // Ex Ey Ez Bx By Bz invvol 0 for every node
   const void* fnode;
+  // max |invvol| (written by pack_nodes): bounds every staged base for the
+  // magic-rint range guard
+  const double* iv_max;
 };
 
 __device__ __forceinline__ unsigned lane_id() {
@@ -80,9 +83,12 @@ __device__ __forceinline__ unsigned lane_id() {
 // policy's compute type.
 template <typename F, typename T>
 __global__ void pack_nodes(const F* __restrict__ E, const F* __restrict__ B,
-                           const F* __restrict__ invvol, int NN, T* __restrict__ out) {
+                           const F* __restrict__ invvol, int NN, T* __restrict__ out,
+                           unsigned long long* iv_max) {
   const int stride = gridDim.x * blockDim.x;
+  double vmax = 0.0;
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < NN; n += stride) {
+    if (invvol) vmax = fmax(vmax, fabs((double)invvol[n]));
     T r[8];
     r[0] = E ? (T)E[n] : T(0);
     r[1] = E ? (T)E[NN + n] : T(0);
@@ -95,6 +101,8 @@ __global__ void pack_nodes(const F* __restrict__ E, const F* __restrict__ B,
 #pragma unroll
     for (int k = 0; k < 8; ++k) out[(size_t)n * 8 + k] = r[k];
   }
+  // non-negative doubles order like their bit patterns
+  if (iv_max && vmax > 0.0) atomicMax(iv_max, (unsigned long long)__double_as_longlong(vmax));
 }
 
 // --------------------------------------------------------------------------
@@ -218,15 +226,14 @@ __device__ __forceinline__ void stage_bases(double* st, const double bs[8]) {
   for (int c = 0; c < 8; ++c) st[c * kRow] = bs[c];
 }
 
-// |value| < 2^50 for every (corner, moment) keeps the magic rint exact
-__device__ __forceinline__ bool magic_unsafe(const double bs[8], double u, double v, double w,
-                                             double uu, double vv, double ww, double lim) {
-  double mb = 0.0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) mb = fmax(mb, fabs(bs[c]));
-  double mm = fmax(1.0, fmax(fabs(u), fmax(fabs(v), fabs(w))));
-  mm = fmax(mm, fmax(uu, fmax(vv, ww)));
-  return !(mb * mm < lim);
+// |base_c * m| < 2^50 for every (corner, moment) keeps the magic rint exact.
+// |base_c| <= |q| * iv_max (weights <= 1) and |m| <= max(1, u^2, v^2, w^2)
+// (|uv| <= max(u^2, v^2)), so one bound per particle suffices; the bound
+// is slightly loose, a failing tile just takes the cvt path.
+__device__ __forceinline__ bool magic_unsafe(double qbound, double uu, double vv, double ww,
+                                             double lim) {
+  const double mm = fmax(1.0, fmax(uu, fmax(vv, ww)));
+  return !(fabs(qbound) * mm < lim);
 }
 
 // Fold one staged tile into the slots.  Lanes are grouped by cell with
@@ -317,13 +324,18 @@ __device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict_
 // SoA loads/stores); every lane of a warp runs the same trip count so warp
 // collectives always see 32 lanes.
 //
-// Policy provides:  P, F, NodeT, kFmaFold,
-//   static int push(const Params&, P& x, P& y, P& z, P& u, P& v, P& w)
-//   static int stage(const Params&, bool valid, P x, P y, P z, P u, P v, P w,
-//                    P q, double* st_bs_lane, double* st_mv_lane, bool& big)
+// Policy provides:  P, F, NodeT, Consts (per-thread constants built from the
+// params once), kFmaFold,
+//   static int push(const Params&, const Consts&, P& x, P& y, P& z, P& u, P& v, P& w)
+//   static int stage(const Params&, const Consts&, bool valid, P x, P y, P z,
+//                    P u, P v, P w, P q, double* st_bs_lane, double* st_mv_lane,
+//                    bool& big)
 //     -> cell key (node index of corner 000) or -1 when outside the box.
+#ifndef BP_MIN_BLOCKS
+#define BP_MIN_BLOCKS 3
+#endif
 template <class Pol, bool DO_PUSH, bool DO_DEPOSIT, bool PRESCALE>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
     span_kernel(SpanParams<typename Pol::P, typename Pol::F> a) {
   typedef typename Pol::P P;
   extern __shared__ double stage_all[];
@@ -342,6 +354,7 @@ __global__ void __launch_bounds__(256, 2)
   const int coff = (lc & 1) * sx + ((lc >> 1) & 1) * sy + ((lc >> 2) & 1);
   const bool third = lg < 2;
   const double sc = a.d.scale;
+  const typename Pol::Consts K(a);  // per-thread constants of the policy
   Slot A{-1, 0, 0, 0, 0}, Bs{-1, 0, 0, 0, 0};
   int worst = ST_OK;
   for (i64 t0 = w0; t0 < w1; t0 += 32) {
@@ -355,7 +368,7 @@ __global__ void __launch_bounds__(256, 2)
       if (DO_DEPOSIT) qp = a.q[p];
     }
     if (DO_PUSH && valid) {
-      const int st = Pol::push(a, xp, yp, zp, un, vn, wn);
+      const int st = Pol::push(a, K, xp, yp, zp, un, vn, wn);
       if (st != ST_OK) {
         worst = st > worst ? st : worst;
         valid = false;
@@ -366,7 +379,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     if (DO_DEPOSIT) {
       bool big = false;
-      const int key = Pol::template stage<PRESCALE>(a, valid, xp, yp, zp, un, vn, wn, qp,
+      const int key = Pol::template stage<PRESCALE>(a, K, valid, xp, yp, zp, un, vn, wn, qp,
                                                     st_bs + lane, st_mv + lane, big);
       if (valid && key < 0) worst = ST_DOMAIN > worst ? ST_DOMAIN : worst;
       __syncwarp();

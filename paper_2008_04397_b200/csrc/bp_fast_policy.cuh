@@ -19,7 +19,10 @@ template <typename T>
 struct FastScalars {
   T o[3], L[3], hi[3], hi2[3], idx[3], ogs[3];
   T dt, dth, qdt2m, beta, beta2, scale;
-  __device__ __forceinline__ explicit FastScalars(const WideScalars& d) {
+  double qlim;  // |q * scale| bound for the magic-rint guard
+  template <typename P, typename F>
+  __device__ __forceinline__ explicit FastScalars(const SpanParams<P, F>& a) {
+    const WideScalars& d = a.d;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       o[k] = (T)d.o[k]; L[k] = (T)d.L[k]; hi[k] = (T)d.hi[k]; hi2[k] = (T)d.hi2[k];
@@ -27,6 +30,7 @@ struct FastScalars {
     }
     dt = (T)d.dt; dth = (T)d.dth; qdt2m = (T)d.qdt2m; beta = (T)d.beta; beta2 = (T)d.beta2;
     scale = (T)d.scale;
+    qlim = (a.iv_max ? __ldg(a.iv_max) : 0.0) * 1.0000001;  // + f32 rounding of the base
   }
 };
 
@@ -66,13 +70,13 @@ __device__ __forceinline__ float fast_rcp(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double fast_rcp(double x) { return __drcp_rn(x); }
 
 // one node record (8 T) -> E, B
-__device__ __forceinline__ void load_record(const float* fn, int n, float e[6]) {
-  const float4* r = reinterpret_cast<const float4*>(fn + (size_t)n * 8);
+__device__ __forceinline__ void load_record(const float* r8, float e[6]) {
+  const float4* r = reinterpret_cast<const float4*>(r8);
   const float4 a = __ldg(r), b = __ldg(r + 1);
   e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w; e[4] = b.x; e[5] = b.y;
 }
-__device__ __forceinline__ void load_record(const double* fn, int n, double e[6]) {
-  const double2* r = reinterpret_cast<const double2*>(fn + (size_t)n * 8);
+__device__ __forceinline__ void load_record(const double* r8, double e[6]) {
+  const double2* r = reinterpret_cast<const double2*>(r8);
   const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
   e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y; e[4] = c.x; e[5] = c.y;
 }
@@ -84,6 +88,7 @@ struct FastPolicy {
   typedef P_ T;
   typedef P_ NodeT;
   static constexpr bool kFmaFold = true;
+  typedef FastScalars<P_> Consts;
 
   static __device__ __forceinline__ int cell_t(const SpanParams<P, F>& a,
                                                const FastScalars<T>& s, T x, T y, T z, T& fx,
@@ -99,9 +104,8 @@ struct FastPolicy {
     return (i * a.NY + j) * a.NZ + k;
   }
 
-  static __device__ __forceinline__ int push(const SpanParams<P, F>& a, P& xp, P& yp, P& zp,
-                                             P& vnx, P& vny, P& vnz) {
-    const FastScalars<T> s(a.d);
+  static __device__ __forceinline__ int push(const SpanParams<P, F>& a, const Consts& s, P& xp,
+                                             P& yp, P& zp, P& vnx, P& vny, P& vnz) {
     const T* fn = static_cast<const T*>(a.fnode);
     const int sx = a.NY * a.NZ, sy = a.NZ;
     T vbx = vnx, vby = vny, vbz = vnz;
@@ -117,13 +121,16 @@ struct FastPolicy {
       const int n000 = cell_t(a, s, xm, ym, zm, fx, fy, fz);
       const T ax = T(1) - fx, ay = T(1) - fy, az = T(1) - fz;
       const T wxy[4] = {ax * ay, fx * ay, ax * fy, fx * fy};
-      const int off[8] = {0, sx, sy, sx + sy, 1, sx + 1, sy + 1, sx + sy + 1};
+      // four record pointers (i/i+1, j/j+1); the k+1 corner is the next record
+      const T* r00 = fn + (size_t)n000 * 8;
+      const T* rr[4] = {r00, r00 + (size_t)sx * 8, r00 + (size_t)sy * 8,
+                        r00 + (size_t)(sx + sy) * 8};
       T e[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const T wc = wxy[c & 3] * ((c & 4) ? fz : az);
         T r[6];
-        load_record(fn, n000 + off[c], r);
+        load_record(rr[c & 3] + ((c & 4) ? 8 : 0), r);
 #pragma unroll
         for (int m = 0; m < 6; ++m) e[m] = fma(wc, r[m], e[m]);
       }
@@ -155,10 +162,9 @@ struct FastPolicy {
   }
 
   template <bool PRESCALE>
-  static __device__ __forceinline__ int stage(const SpanParams<P, F>& a, bool valid, P xp, P yp,
-                                              P zp, P un, P vn, P wn, P qp, double* st_bs,
-                                              double* st_mv, bool& big) {
-    const FastScalars<T> s(a.d);
+  static __device__ __forceinline__ int stage(const SpanParams<P, F>& a, const Consts& s,
+                                              bool valid, P xp, P yp, P zp, P un, P vn, P wn,
+                                              P qp, double* st_bs, double* st_mv, bool& big) {
     const T* fn = static_cast<const T*>(a.fnode);
     const int sx = a.NY * a.NZ, sy = a.NZ;
     int key = -1;
@@ -174,11 +180,13 @@ struct FastPolicy {
     const T qs = key >= 0 ? qp * s.scale : T(0);  // the lattice scale is folded in once
     const T ax = T(1) - fx, ay = T(1) - fy, az = T(1) - fz;
     const T wxy[4] = {ax * ay, fx * ay, ax * fy, fx * fy};
-    const int off[8] = {0, sx, sy, sx + sy, 1, sx + 1, sy + 1, sx + sy + 1};
+    const T* r00 = fn + (size_t)nb * 8 + 6;
+    const T* rr[4] = {r00, r00 + (size_t)sx * 8, r00 + (size_t)sy * 8,
+                      r00 + (size_t)(sx + sy) * 8};
     double bs[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const T iv = __ldg(fn + (size_t)(nb + off[c]) * 8 + 6);
+      const T iv = __ldg(rr[c & 3] + ((c & 4) ? 8 : 0));
       bs[c] = (double)(qs * (wxy[c & 3] * ((c & 4) ? fz : az)) * iv);
     }
     stage_bases(st_bs, bs);
@@ -186,8 +194,8 @@ struct FastPolicy {
     const T pyy = vn * vn, pyz = vn * wn, pzz = wn * wn;
     stage_moments(st_mv, (double)un, (double)vn, (double)wn, (double)pxx, (double)pxy,
                   (double)pxz, (double)pyy, (double)pyz, (double)pzz);
-    big = key >= 0 && magic_unsafe(bs, (double)un, (double)vn, (double)wn, (double)pxx,
-                                   (double)pyy, (double)pzz, kMagicLimit);
+    big = key >= 0 && magic_unsafe((double)qs * s.qlim, (double)pxx, (double)pyy, (double)pzz,
+                                   kMagicLimit);
     return key;
   }
 };

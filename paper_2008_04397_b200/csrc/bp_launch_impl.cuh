@@ -54,6 +54,7 @@ SpanParams<P, F> make_params(const Call& c) {
   a.d.dt = (double)a.dt; a.d.dth = (double)a.dth; a.d.qdt2m = (double)a.qdt2m;
   a.d.beta = (double)a.beta; a.d.one = (double)a.one; a.d.two = (double)a.two;
   a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
+  a.iv_max = nullptr;
   return a;
 }
 
@@ -119,14 +120,18 @@ int run_span(const Call& c, bool prescale_ok, cudaStream_t s) {
   typedef typename Pol::NodeT T;
   auto a = make_params<P, F>(c);
   T* fn = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&fn, (size_t)a.NN * 8 * sizeof(T), s);
+  const size_t rec_bytes = ((size_t)a.NN * 8 * sizeof(T) + 255) & ~(size_t)255;
+  cudaError_t e = cudaMallocAsync((void**)&fn, rec_bytes + 256, s);
   if (e != cudaSuccess) {
     set_error("node record alloc: %s", cudaGetErrorString(e));
     return -2;
   }
+  unsigned long long* ivm = reinterpret_cast<unsigned long long*>((char*)fn + rec_bytes);
+  cudaMemsetAsync(ivm, 0, sizeof(unsigned long long), s);
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
   pack_nodes<F, T><<<pb, 256, 0, s>>>(PUSH ? a.E : nullptr, PUSH ? a.B : nullptr,
-                                      DEP ? a.invvol : nullptr, a.NN, fn);
+                                      DEP ? a.invvol : nullptr, a.NN, fn, ivm);
+  a.iv_max = reinterpret_cast<const double*>(ivm);
   note_launch();
   a.fnode = fn;
   int rc;

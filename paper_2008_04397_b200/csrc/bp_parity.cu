@@ -17,7 +17,7 @@ int run_gather(const Call& c, cudaStream_t s) {
     return -2;
   }
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
-  pack_nodes<F, double><<<pb, 256, 0, s>>>(a.E, a.B, (const F*)nullptr, a.NN, fn);
+  pack_nodes<F, double><<<pb, 256, 0, s>>>(a.E, a.B, (const F*)nullptr, a.NN, fn, nullptr);
   note_launch();
   a.fnode = fn;
   const int grid = grid_for(gather_kernel<P, F>, 0, c.count, kThreads);

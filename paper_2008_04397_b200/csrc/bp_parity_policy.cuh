@@ -81,10 +81,15 @@ struct ParityPolicy {
   typedef F_ F;
   typedef double NodeT;
   static constexpr bool kFmaFold = false;
+  struct Consts {
+    double iv_max;
+    __device__ __forceinline__ explicit Consts(const SpanParams<P, F>& a)
+        : iv_max(a.iv_max ? __ldg(a.iv_max) : 0.0) {}
+  };
 
   // Push block for one particle (kernels.py:489-682), in place on OK.
-  static __device__ __forceinline__ int push(const SpanParams<P, F>& a, P& xp, P& yp, P& zp,
-                                             P& vnx, P& vny, P& vnz) {
+  static __device__ __forceinline__ int push(const SpanParams<P, F>& a, const Consts&, P& xp,
+                                             P& yp, P& zp, P& vnx, P& vny, P& vnz) {
     const auto& d = a.d;
     const double* fn = static_cast<const double*>(a.fnode);
     double vbx = (double)vnx, vby = (double)vny, vbz = (double)vnz;
@@ -176,9 +181,9 @@ struct ParityPolicy {
 
   // Deposit values of one particle (kernels.py:683-734), staged as doubles.
   template <bool PRESCALE>
-  static __device__ __forceinline__ int stage(const SpanParams<P, F>& a, bool valid, P xp, P yp,
-                                              P zp, P un, P vn, P wn, P qp, double* st_bs,
-                                              double* st_mv, bool& big) {
+  static __device__ __forceinline__ int stage(const SpanParams<P, F>& a, const Consts& K,
+                                              bool valid, P xp, P yp, P zp, P un, P vn, P wn,
+                                              P qp, double* st_bs, double* st_mv, bool& big) {
     double fx = 0, fy = 0, fz = 0;
     int key = valid ? cell(a, xp, yp, zp, fx, fy, fz) : -1;
     // invalid particles stage zero bases: folding them adds exact zeros
@@ -202,7 +207,7 @@ struct ParityPolicy {
     const P pyy = vn * vn, pyz = vn * wn, pzz = wn * wn;
     stage_moments(st_mv, (double)un, (double)vn, (double)wn, (double)pxx, (double)pxy,
                   (double)pxz, (double)pyy, (double)pyz, (double)pzz);
-    big = key >= 0 && magic_unsafe(bs, (double)un, (double)vn, (double)wn, (double)pxx,
+    big = key >= 0 && magic_unsafe(q * K.iv_max * (PRESCALE ? a.d.scale : 1.0), (double)pxx,
                                    (double)pyy, (double)pzz,
                                    PRESCALE ? kMagicLimit : kMagicLimit / a.d.scale);
     return key;
