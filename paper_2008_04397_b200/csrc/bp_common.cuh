@@ -42,6 +42,13 @@ struct WideScalars {
   double dt, dth, qdt2m, beta, one, two, beta2, scale;
 };
 
+// The fast arithmetic's constants rounded once to f32 on the host, read
+// straight from the parameter bank by FFMA/FSETP.
+struct NarrowScalars {
+  float o[3], L[3], hi[3], hi2[3], idx[3], ogs[3];
+  float dt, dth, qdt2m, beta, beta2, scale;
+};
+
 template <typename P, typename F>
 struct SpanParams {
   P *x, *y, *z, *u, *v, *w;
@@ -60,6 +67,7 @@ struct SpanParams {
   P dt, dth, qdt2m, beta, one, two, beta2;
   F scale;
   WideScalars d;
+  NarrowScalars f;
   int n_iters, mixed, apply_bc;
   int* status;
   P* gather_out;  // gather only: (count, 6)
@@ -69,7 +77,61 @@ struct SpanParams {
   // max |invvol| (written by pack_nodes): bounds every staged base for the
   // magic-rint range guard
   const double* iv_max;
+  // every full 32-particle tile of the span is 16-byte aligned in all arrays:
+  // tiles stream through shared memory with TMA bulk copies
+  int bulk;
 };
+
+// ---- TMA bulk copies and mbarriers (sm_90+ PTX, UBLKCP in SASS) ----------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 __device__ __forceinline__ unsigned lane_id() {
   unsigned r;
@@ -137,6 +199,11 @@ constexpr int kRow = 34;
 constexpr int kStageBs = 8 * kRow;
 constexpr int kStageMv = 12 * kRow;
 constexpr int kWarpStage = kStageBs + kStageMv;
+// particle tiles: 2 stages x 7 arrays x 32 particles of P, + 2 mbarriers
+template <typename P>
+__host__ __device__ constexpr int warp_smem_doubles() {
+  return kWarpStage + (2 * 7 * 32 * (int)sizeof(P)) / 8 + 2;
+}
 
 // Exact rint without the conversion pipe: for |t| < 2^51, t + 1.5*2^52 lands
 // in [2^52, 2^53) where the ulp is 1, so the FP add rounds t half-to-even
@@ -346,8 +413,14 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
   const i64 per = ((a.count + nwarps - 1) / nwarps + 31) & ~(i64)31;
   const i64 w0 = gw * per;
   const i64 w1 = w0 + per < a.count ? w0 + per : a.count;
-  double* const st_bs = stage_all + (size_t)wib * kWarpStage;
+  // per-warp shared memory: deposit staging [+ particle tile stages when bulk]
+  double* const st_bs =
+      stage_all + (size_t)wib * (a.bulk ? warp_smem_doubles<P>() : kWarpStage);
   double* const st_mv = st_bs + kStageBs;
+  // particle tile stages [2][7][32] of P, then the 2 mbarriers
+  P* const tiles = reinterpret_cast<P*>(st_bs + kWarpStage);
+  unsigned long long* const bars = reinterpret_cast<unsigned long long*>(
+      st_bs + kWarpStage + (2 * 7 * 32 * (int)sizeof(P)) / 8);
   const int sx = a.NY * a.NZ, sy = a.NZ;
   // this lane's share of the 80 sums
   const int lc = lane & 7, lg = lane >> 3;
@@ -357,24 +430,80 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
   const typename Pol::Consts K(a);  // per-thread constants of the policy
   Slot A{-1, 0, 0, 0, 0}, Bs{-1, 0, 0, 0, 0};
   int worst = ST_OK;
-  for (i64 t0 = w0; t0 < w1; t0 += 32) {
+  // Particle SoA streams: full tiles move HBM <-> shared memory with TMA bulk
+  // copies (one elected lane, 128/256-byte transfers per array, the next
+  // tile's load in flight while this one is computed); a ragged last tile or
+  // an unaligned span uses plain coalesced loads/stores.
+  P* const arr[7] = {a.x, a.y, a.z, a.u, a.v, a.w, const_cast<P*>(a.q)};
+  const int narr = DO_DEPOSIT ? 7 : 6;
+  const unsigned tile_bytes = 32 * sizeof(P);
+  if (a.bulk && lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  auto full = [&](i64 t) { return a.bulk && t + 32 <= w1; };
+  auto issue = [&](i64 t, int stg) {
+    if (lane == 0) {
+      mbar_expect_tx(bars + stg, narr * tile_bytes);
+      for (int k = 0; k < narr; ++k)
+        bulk_load(tiles + (stg * 7 + k) * 32, arr[k] + a.start + t, tile_bytes, bars + stg);
+    }
+  };
+  if (w0 < w1 && full(w0)) issue(w0, 0);
+  unsigned phase = 0;  // bit s: parity of stage s's next completion
+  int it = 0;
+  for (i64 t0 = w0; t0 < w1; t0 += 32, ++it) {
+    const int stg = it & 1;
     const i64 r = t0 + lane;
     bool valid = r < w1;
     const i64 p = a.start + r;
-    P xp = 0, yp = 0, zp = 0, un = 0, vn = 0, wn = 0, qp = 0;
-    if (valid) {
-      xp = a.x[p]; yp = a.y[p]; zp = a.z[p];
-      un = a.u[p]; vn = a.v[p]; wn = a.w[p];
-      if (DO_DEPOSIT) qp = a.q[p];
+    const bool cur_full = full(t0);
+    if (full(t0 + 32)) {
+      // the other stage held tile it-1: its bulk store must have read it
+      if (DO_PUSH && lane == 0) bulk_wait_read_all();
+      __syncwarp();
+      issue(t0 + 32, stg ^ 1);
     }
-    if (DO_PUSH && valid) {
-      const int st = Pol::push(a, K, xp, yp, zp, un, vn, wn);
-      if (st != ST_OK) {
-        worst = st > worst ? st : worst;
-        valid = false;
-      } else {
-        a.x[p] = xp; a.y[p] = yp; a.z[p] = zp;
-        a.u[p] = un; a.v[p] = vn; a.w[p] = wn;
+    P xp = 0, yp = 0, zp = 0, un = 0, vn = 0, wn = 0, qp = 0;
+    P* const cur = tiles + stg * 7 * 32;
+    if (cur_full) {
+      mbar_wait(bars + stg, (phase >> stg) & 1u);
+      phase ^= 1u << stg;
+      xp = cur[0 * 32 + lane]; yp = cur[1 * 32 + lane]; zp = cur[2 * 32 + lane];
+      un = cur[3 * 32 + lane]; vn = cur[4 * 32 + lane]; wn = cur[5 * 32 + lane];
+      if (DO_DEPOSIT) qp = cur[6 * 32 + lane];
+    } else if (valid) {
+      // streamed once: evict-first so the field records keep L1
+      xp = __ldcs(a.x + p); yp = __ldcs(a.y + p); zp = __ldcs(a.z + p);
+      un = __ldcs(a.u + p); vn = __ldcs(a.v + p); wn = __ldcs(a.w + p);
+      if (DO_DEPOSIT) qp = __ldcs(a.q + p);
+    }
+    if (DO_PUSH) {
+      if (valid) {
+        const int st = Pol::push(a, K, xp, yp, zp, un, vn, wn);
+        if (st != ST_OK) {
+          // not stored, not deposited (kernels.py:618-621, 672-676); a bulk
+          // store writes the tile's loaded values back unchanged
+          worst = st > worst ? st : worst;
+          valid = false;
+        } else if (cur_full) {
+          cur[0 * 32 + lane] = xp; cur[1 * 32 + lane] = yp; cur[2 * 32 + lane] = zp;
+          cur[3 * 32 + lane] = un; cur[4 * 32 + lane] = vn; cur[5 * 32 + lane] = wn;
+        } else {
+          __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
+          __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
+        }
+      }
+      if (cur_full) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          for (int k = 0; k < 6; ++k)
+            bulk_store(arr[k] + a.start + t0, cur + k * 32, tile_bytes);
+          bulk_commit();
+        }
       }
     }
     if (DO_DEPOSIT) {
@@ -392,6 +521,7 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
     slot_flush(A, a.acc, a.NN, lg, coff, third);
     slot_flush(Bs, a.acc, a.NN, lg, coff, third);
   }
+  if (DO_PUSH && a.bulk && lane == 0) bulk_wait_all();
   if (worst != ST_OK) atomicMax(a.status, worst);
 }
 

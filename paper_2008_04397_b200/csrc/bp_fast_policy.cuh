@@ -15,23 +15,51 @@
 
 namespace bp {
 
+// Per-thread constants of the fast arithmetic.  f32: read from the host-
+// rounded parameter copy (no per-particle conversions); f64: the wide copy.
 template <typename T>
-struct FastScalars {
-  T o[3], L[3], hi[3], hi2[3], idx[3], ogs[3];
-  T dt, dth, qdt2m, beta, beta2, scale;
+struct FastScalars;
+
+template <>
+struct FastScalars<float> {
+  const NarrowScalars& f;
   double qlim;  // |q * scale| bound for the magic-rint guard
   template <typename P, typename F>
-  __device__ __forceinline__ explicit FastScalars(const SpanParams<P, F>& a) {
-    const WideScalars& d = a.d;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      o[k] = (T)d.o[k]; L[k] = (T)d.L[k]; hi[k] = (T)d.hi[k]; hi2[k] = (T)d.hi2[k];
-      idx[k] = (T)d.inv_gd[k]; ogs[k] = (T)d.go_s[k];
-    }
-    dt = (T)d.dt; dth = (T)d.dth; qdt2m = (T)d.qdt2m; beta = (T)d.beta; beta2 = (T)d.beta2;
-    scale = (T)d.scale;
-    qlim = (a.iv_max ? __ldg(a.iv_max) : 0.0) * 1.0000001;  // + f32 rounding of the base
-  }
+  __device__ __forceinline__ explicit FastScalars(const SpanParams<P, F>& a)
+      : f(a.f), qlim((a.iv_max ? __ldg(a.iv_max) : 0.0) * 1.0000001) {}
+  __device__ __forceinline__ float o(int k) const { return f.o[k]; }
+  __device__ __forceinline__ float L(int k) const { return f.L[k]; }
+  __device__ __forceinline__ float hi(int k) const { return f.hi[k]; }
+  __device__ __forceinline__ float hi2(int k) const { return f.hi2[k]; }
+  __device__ __forceinline__ float idx(int k) const { return f.idx[k]; }
+  __device__ __forceinline__ float ogs(int k) const { return f.ogs[k]; }
+  __device__ __forceinline__ float dt() const { return f.dt; }
+  __device__ __forceinline__ float dth() const { return f.dth; }
+  __device__ __forceinline__ float qdt2m() const { return f.qdt2m; }
+  __device__ __forceinline__ float beta() const { return f.beta; }
+  __device__ __forceinline__ float beta2() const { return f.beta2; }
+  __device__ __forceinline__ float scale() const { return f.scale; }
+};
+
+template <>
+struct FastScalars<double> {
+  const WideScalars& d;
+  double qlim;
+  template <typename P, typename F>
+  __device__ __forceinline__ explicit FastScalars(const SpanParams<P, F>& a)
+      : d(a.d), qlim(a.iv_max ? __ldg(a.iv_max) : 0.0) {}
+  __device__ __forceinline__ double o(int k) const { return d.o[k]; }
+  __device__ __forceinline__ double L(int k) const { return d.L[k]; }
+  __device__ __forceinline__ double hi(int k) const { return d.hi[k]; }
+  __device__ __forceinline__ double hi2(int k) const { return d.hi2[k]; }
+  __device__ __forceinline__ double idx(int k) const { return d.inv_gd[k]; }
+  __device__ __forceinline__ double ogs(int k) const { return d.go_s[k]; }
+  __device__ __forceinline__ double dt() const { return d.dt; }
+  __device__ __forceinline__ double dth() const { return d.dth; }
+  __device__ __forceinline__ double qdt2m() const { return d.qdt2m; }
+  __device__ __forceinline__ double beta() const { return d.beta; }
+  __device__ __forceinline__ double beta2() const { return d.beta2; }
+  __device__ __forceinline__ double scale() const { return d.scale; }
 };
 
 template <typename T>
@@ -93,9 +121,9 @@ struct FastPolicy {
   static __device__ __forceinline__ int cell_t(const SpanParams<P, F>& a,
                                                const FastScalars<T>& s, T x, T y, T z, T& fx,
                                                T& fy, T& fz) {
-    const T gx = fma(x, s.idx[0], -s.ogs[0]);
-    const T gy = fma(y, s.idx[1], -s.ogs[1]);
-    const T gz = fma(z, s.idx[2], -s.ogs[2]);
+    const T gx = fma(x, s.idx(0), -s.ogs(0));
+    const T gy = fma(y, s.idx(1), -s.ogs(1));
+    const T gz = fma(z, s.idx(2), -s.ogs(2));
     int i = (int)gx, j = (int)gy, k = (int)gz;
     i = i < 0 ? 0 : (i > a.nx - 1 ? a.nx - 1 : i);
     j = j < 0 ? 0 : (j > a.ny - 1 ? a.ny - 1 : j);
@@ -110,12 +138,12 @@ struct FastPolicy {
     const int sx = a.NY * a.NZ, sy = a.NZ;
     T vbx = vnx, vby = vny, vbz = vnz;
     for (int it = 0; it < a.n_iters; ++it) {
-      T xm = fma(vbx, s.dth, xp), ym = fma(vby, s.dth, yp), zm = fma(vbz, s.dth, zp);
-      xm = fold_mid_t(xm, s.o[0], s.L[0], s.hi[0], s.hi2[0], a.bcx);
-      ym = fold_mid_t(ym, s.o[1], s.L[1], s.hi[1], s.hi2[1], a.bcy);
-      zm = fold_mid_t(zm, s.o[2], s.L[2], s.hi[2], s.hi2[2], a.bcz);
-      if (xm < s.o[0] || xm > s.hi[0] || ym < s.o[1] || ym > s.hi[1] || zm < s.o[2] ||
-          zm > s.hi[2])
+      T xm = fma(vbx, s.dth(), xp), ym = fma(vby, s.dth(), yp), zm = fma(vbz, s.dth(), zp);
+      xm = fold_mid_t(xm, s.o(0), s.L(0), s.hi(0), s.hi2(0), a.bcx);
+      ym = fold_mid_t(ym, s.o(1), s.L(1), s.hi(1), s.hi2(1), a.bcy);
+      zm = fold_mid_t(zm, s.o(2), s.L(2), s.hi(2), s.hi2(2), a.bcz);
+      if (xm < s.o(0) || xm > s.hi(0) || ym < s.o(1) || ym > s.hi(1) || zm < s.o(2) ||
+          zm > s.hi(2))
         return ST_MIDPOINT;
       T fx, fy, fz;
       const int n000 = cell_t(a, s, xm, ym, zm, fx, fy, fz);
@@ -134,26 +162,26 @@ struct FastPolicy {
 #pragma unroll
         for (int m = 0; m < 6; ++m) e[m] = fma(wc, r[m], e[m]);
       }
-      const T tx = fma(s.qdt2m, e[0], vnx), ty = fma(s.qdt2m, e[1], vny),
-              tz = fma(s.qdt2m, e[2], vnz);
+      const T tx = fma(s.qdt2m(), e[0], vnx), ty = fma(s.qdt2m(), e[1], vny),
+              tz = fma(s.qdt2m(), e[2], vnz);
       const T hx = e[3], hy = e[4], hz = e[5];
       const T bsq = fma(hx, hx, fma(hy, hy, hz * hz));
-      const T inv = fast_rcp(fma(s.beta2, bsq, T(1)));
+      const T inv = fast_rcp(fma(s.beta2(), bsq, T(1)));
       const T tdb = fma(tx, hx, fma(ty, hy, tz * hz));
-      const T bt = s.beta * tdb;
+      const T bt = s.beta() * tdb;
       const T cx = fma(ty, hz, -tz * hy), cy = fma(tz, hx, -tx * hz), cz = fma(tx, hy, -ty * hx);
-      vbx = fma(s.beta, fma(bt, hx, cx), tx) * inv;
-      vby = fma(s.beta, fma(bt, hy, cy), ty) * inv;
-      vbz = fma(s.beta, fma(bt, hz, cz), tz) * inv;
+      vbx = fma(s.beta(), fma(bt, hx, cx), tx) * inv;
+      vby = fma(s.beta(), fma(bt, hy, cy), ty) * inv;
+      vbz = fma(s.beta(), fma(bt, hz, cz), tz) * inv;
     }
-    T xo = fma(vbx, s.dt, xp), yo = fma(vby, s.dt, yp), zo = fma(vbz, s.dt, zp);
+    T xo = fma(vbx, s.dt(), xp), yo = fma(vby, s.dt(), yp), zo = fma(vbz, s.dt(), zp);
     T uo = T(2) * vbx - vnx, vo = T(2) * vby - vny, wo = T(2) * vbz - vnz;
     if (a.apply_bc) {
-      fold_commit_t(xo, uo, s.o[0], s.L[0], s.hi[0], s.hi2[0], a.bcx);
-      fold_commit_t(yo, vo, s.o[1], s.L[1], s.hi[1], s.hi2[1], a.bcy);
-      fold_commit_t(zo, wo, s.o[2], s.L[2], s.hi[2], s.hi2[2], a.bcz);
-      if (xo < s.o[0] || xo > s.hi[0] || yo < s.o[1] || yo > s.hi[1] || zo < s.o[2] ||
-          zo > s.hi[2])
+      fold_commit_t(xo, uo, s.o(0), s.L(0), s.hi(0), s.hi2(0), a.bcx);
+      fold_commit_t(yo, vo, s.o(1), s.L(1), s.hi(1), s.hi2(1), a.bcy);
+      fold_commit_t(zo, wo, s.o(2), s.L(2), s.hi(2), s.hi2(2), a.bcz);
+      if (xo < s.o(0) || xo > s.hi(0) || yo < s.o(1) || yo > s.hi(1) || zo < s.o(2) ||
+          zo > s.hi(2))
         return ST_RUNAWAY;
     }
     xp = xo; yp = yo; zp = zo;
@@ -172,12 +200,12 @@ struct FastPolicy {
     if (valid) {
       // domain check as in the reference deposit (positions are in the box
       // after the push; a deposit-only call may hand us anything)
-      if (xp >= s.o[0] && xp <= s.hi[0] && yp >= s.o[1] && yp <= s.hi[1] && zp >= s.o[2] &&
-          zp <= s.hi[2])
+      if (xp >= s.o(0) && xp <= s.hi(0) && yp >= s.o(1) && yp <= s.hi(1) && zp >= s.o(2) &&
+          zp <= s.hi(2))
         key = cell_t(a, s, xp, yp, zp, fx, fy, fz);
     }
     const int nb = key >= 0 ? key : 0;
-    const T qs = key >= 0 ? qp * s.scale : T(0);  // the lattice scale is folded in once
+    const T qs = key >= 0 ? qp * s.scale() : T(0);  // the lattice scale is folded in once
     const T ax = T(1) - fx, ay = T(1) - fy, az = T(1) - fz;
     const T wxy[4] = {ax * ay, fx * ay, ax * fy, fx * fy};
     const T* r00 = fn + (size_t)nb * 8 + 6;

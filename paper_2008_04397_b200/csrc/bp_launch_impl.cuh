@@ -4,6 +4,7 @@
 #pragma once
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "bp_common.cuh"
 #include "bp_launch.h"
@@ -55,11 +56,29 @@ SpanParams<P, F> make_params(const Call& c) {
   a.d.beta = (double)a.beta; a.d.one = (double)a.one; a.d.two = (double)a.two;
   a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
   a.iv_max = nullptr;
+  {
+    // TMA bulk tiles need every full tile 16-byte aligned in all 7 arrays
+    const void* ptrs[7] = {c.x, c.y, c.z, c.u, c.v, c.w, c.q};
+    bool ok = ((c.start * (int64_t)sizeof(P)) % 16) == 0;
+    for (int k = 0; k < 7; ++k)
+      if (ptrs[k] && ((uintptr_t)ptrs[k] % 16) != 0) ok = false;
+    if (!c.x || !c.u || (c.op != OP_PUSH && !c.q)) ok = false;
+    // opt-in: measured slower on B200 at C3 (its shared memory is taken from
+    // the L1 that serves the field gathers), see DESIGN.md
+    const char* env = getenv("BP_TMA_STREAM");
+    a.bulk = (ok && env && env[0] == '1') ? 1 : 0;
+  }
+  for (int k = 0; k < 3; ++k) {
+    a.f.o[k] = (float)a.d.o[k]; a.f.L[k] = (float)a.d.L[k];
+    a.f.hi[k] = (float)a.d.hi[k]; a.f.hi2[k] = (float)a.d.hi2[k];
+    a.f.idx[k] = (float)a.d.inv_gd[k]; a.f.ogs[k] = (float)a.d.go_s[k];
+  }
+  a.f.dt = (float)a.d.dt; a.f.dth = (float)a.d.dth; a.f.qdt2m = (float)a.d.qdt2m;
+  a.f.beta = (float)a.d.beta; a.f.beta2 = (float)a.d.beta2; a.f.scale = (float)a.d.scale;
   return a;
 }
 
 constexpr int kThreads = 256;
-constexpr size_t kSmem = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
 
 inline int sm_count() {
   static int sms = 0;
@@ -100,14 +119,20 @@ template <class Pol, bool PUSH, bool DEP, bool PRE>
 int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t count,
                 cudaStream_t s) {
   auto k = span_kernel<Pol, PUSH, DEP, PRE>;
+  // deposit staging always; the particle tile stages only on the TMA path
+  // (the rest of the SM's shared memory stays L1 for the field gathers)
+  constexpr size_t kFull =
+      (size_t)(kThreads / 32) * warp_smem_doubles<typename Pol::P>() * sizeof(double);
+  constexpr size_t kStageOnly = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
+  const size_t smem = a.bulk ? kFull : kStageOnly;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFull);
     attr = true;
   }
   // one wave of resident blocks; every warp walks a contiguous run of >= 32
-  const int grid = grid_for(k, kSmem, count, kThreads);
-  k<<<grid, kThreads, kSmem, s>>>(a);
+  const int grid = grid_for(k, smem, count, kThreads);
+  k<<<grid, kThreads, smem, s>>>(a);
   note_launch();
   return launch_error("span kernel launch");
 }

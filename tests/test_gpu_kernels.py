@@ -220,3 +220,47 @@ def test_fast_arith_deposit_is_order_independent(gpu):
         K.deposit_span(*d, 0, n, dacc, dinv, geo_g, geo_i, fd(1.0), fd(SCALE))
         out.append(dacc.cpu().numpy())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.fixture
+def tma_stream(monkeypatch):
+    """Route full particle tiles through the TMA bulk-copy path."""
+    monkeypatch.setenv("BP_TMA_STREAM", "1")
+    yield
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("arith", ["parity", "fast"])
+def test_tma_stream_path_matches(gpu, oracle, tma_stream, monkeypatch, mode, arith):
+    """The bulk-copy (UBLKCP) streaming path gives the same bits as the plain
+    path: bitwise vs the oracle in parity arithmetic, and identical to the
+    plain fast path in fast arithmetic (a span with an unaligned start and a
+    ragged tail exercises the fallback tiles)."""
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 100_003
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(mode, n, seed=29,
+                                                                       order="sorted")
+    inv = geom.inv_node_volume(fd)
+    mixed = 1 if pd != fd else 0
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+            fd(SCALE), mixed)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    for start in (0, 3):
+        count = n - start
+        out = []
+        for env in ("1", "0"):
+            monkeypatch.setenv("BP_TMA_STREAM", env)
+            d = _dev(torch, arrs)
+            dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+            st = K.fused_span(*d, start, count, dE, dB, dacc, dinv, *tail, arith=arith)
+            out.append((st, dacc, d))
+        (st, dacc, d), (st2, dacc2, d2) = out
+        assert st == st2 and torch.equal(dacc, dacc2)
+        assert all(torch.equal(a, b) for a, b in zip(d, d2))
+        if arith == "parity":
+            ref = [a.copy() for a in arrs]
+            acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+            oracle.fused_span(*ref, start, count, E, B, acc_ref, inv, *tail)
+            assert np.array_equal(acc_ref, dacc.cpu().numpy())
+            assert all(np.array_equal(r, t.cpu().numpy()) for r, t in zip(ref, d))
