@@ -200,3 +200,34 @@ def sample_host(geom, species, cells, init=GemInit(), precision=None, c=1.0, see
         out.append(ParticleBuffer(*(a.astype(pd) for a in pos + vel + [q]),
                                   ids=np.arange(n, dtype=np.int64), species_id=s.species_id))
     return out
+
+
+def init_uniform_device(geom, species, device, n0=1.0, precision=None, cells=None, seed=1):
+    """Uniform drifting-Maxwellian plasma in HBM (the reference's
+    ``init.kind = uniform`` loader, pipeline.py:140-151, with torch's device
+    RNG): ppc particles per cell, cell-major, charge weight
+    q * n0 * V_cell / ppc."""
+    import torch
+    mode = precision or PrecisionMode()
+    pdt = torch.float32 if mode.particle_dtype == np.float32 else torch.float64
+    c0, nc = (0, geom.n_cells) if cells is None else cells
+    out = []
+    for s in species:
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + s.species_id * 7919 + c0)
+        n = nc * s.ppc
+        lin = torch.arange(c0, c0 + nc, device=device, dtype=torch.int64)
+        idx = (lin % geom.nx, (lin // geom.nx) % geom.ny, lin // (geom.nx * geom.ny))
+        arrs = []
+        for a, cidx in enumerate(idx):
+            d, o = geom.spacings[a], geom.origin[a]
+            jit = torch.rand(n, device=device, dtype=torch.float64, generator=g)
+            arrs.append((o + d * cidx.repeat_interleave(s.ppc).to(torch.float64) + d * jit).to(pdt))
+        for a in range(3):
+            nrm = torch.randn(n, device=device, dtype=torch.float64, generator=g)
+            arrs.append((s.drift[a] + s.vth[a] * nrm).to(pdt))
+        arrs.append(torch.full((n,), s.charge * n0 * geom.cell_volume / s.ppc, device=device,
+                               dtype=pdt))
+        ids = torch.arange(c0 * s.ppc, (c0 + nc) * s.ppc, device=device, dtype=torch.int64)
+        out.append(DeviceParticles(*arrs, ids, species_id=s.species_id))
+    return out
