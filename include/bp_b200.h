@@ -137,6 +137,15 @@ int bp_sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs
                     void* qs, int64_t* ids, int64_t n, const double* origin,
                     const double* spacing, const int64_t* counts, void* stream);
 
+/* Sorted copy: src[0..6] = x y z u v w q (q may be NULL), src_ids (may be
+ * NULL) are read, their cell-sorted permutation (same order as
+ * bp_sort_by_cell) is written to the distinct arrays dst / dst_ids — one
+ * fused gather pass and no copy back, for callers that keep a spare buffer
+ * set and swap.  On BP_ERR_DOMAIN, dst is unspecified and src untouched. */
+int bp_sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* const* dst,
+                         int64_t* dst_ids, int64_t n, const double* origin,
+                         const double* spacing, const int64_t* counts, void* stream);
+
 /* Linear cell key per particle (geometry.cell_index_of) into keys[n] (device
  * int64).  Returns BP_ERR_DOMAIN on positions below the origin. */
 int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,

@@ -26,7 +26,7 @@ ARITH_FAST = 1
 EXPORTS = (
     "bp_version", "bp_last_error", "bp_kernel_launches", "bp_fused_span", "bp_push_span",
     "bp_deposit_span", "bp_gather_span", "bp_fused_span_ex",
-    "bp_fused_span_host", "bp_sort_by_cell", "bp_cell_keys",
+    "bp_fused_span_host", "bp_sort_by_cell", "bp_sort_by_cell_into", "bp_cell_keys",
     "bp_fold_periodic_i64",
 )
 
@@ -54,6 +54,7 @@ _SIGS = {
                            + [_P] * 4 + [_P, _P, _P] + [_D] * 5
                            + [_INT, _D, _INT, _I64]),
     "bp_sort_by_cell": (_INT, [_INT] + [_P] * 7 + [_P, _I64, _P, _P, _P, _P]),
+    "bp_sort_by_cell_into": (_INT, [_INT, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "bp_cell_keys": (_INT, [_INT, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "bp_fold_periodic_i64": (_INT, [_P, _I64, _P, _P]),
 }

@@ -51,6 +51,9 @@ int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, v
                  void* qs, int64_t* ids, int64_t n, const double* origin,
                  const double* spacing, const int64_t* counts, cudaStream_t s);
 int fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, cudaStream_t s);
+int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* const* dst,
+                      int64_t* dst_ids, int64_t n, const double* origin, const double* spacing,
+                      const int64_t* counts, cudaStream_t s);
 
 namespace {
 
@@ -433,6 +436,27 @@ int bp_sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs
   ensure_pool();
   return sort_by_cell(pbytes, xs, ys, zs, us, vs, ws, qs, ids, n, origin, spacing, counts,
                       (cudaStream_t)stream);
+}
+
+int bp_sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* const* dst,
+                         int64_t* dst_ids, int64_t n, const double* origin,
+                         const double* spacing, const int64_t* counts, void* stream) {
+  if (pbytes != 4 && pbytes != 8) {
+    set_error("unsupported particle dtype (%d bytes)", pbytes);
+    return BP_EINVAL;
+  }
+  if (!src || !dst) {
+    set_error("src and dst arrays are required");
+    return BP_EINVAL;
+  }
+  for (int k = 0; k < 6; ++k)
+    if (!src[k] || !dst[k] || src[k] == dst[k]) {
+      set_error("sort_by_cell_into needs distinct source and destination arrays");
+      return BP_EINVAL;
+    }
+  ensure_pool();
+  return sort_by_cell_into(pbytes, src, src_ids, dst, dst_ids, n, origin, spacing, counts,
+                           (cudaStream_t)stream);
 }
 
 int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,

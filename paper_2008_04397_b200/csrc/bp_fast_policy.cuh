@@ -94,7 +94,9 @@ __device__ __forceinline__ void fold_commit_t(T& q, T& vel, T o, T L, T hi, T hi
   }
 }
 
-__device__ __forceinline__ float fast_rcp(float x) { return __frcp_rn(x); }
+// 1 / denom with denom = 1 + beta^2 |h|^2 >= 1: MUFU.RCP (2 ulp) is ample
+// against the 1e-4 tolerance of the f32 path
+__device__ __forceinline__ float fast_rcp(float x) { return __fdividef(1.0f, x); }
 __device__ __forceinline__ double fast_rcp(double x) { return __drcp_rn(x); }
 
 // one node record (8 T) -> E, B
@@ -125,9 +127,11 @@ struct FastPolicy {
     const T gy = fma(y, s.idx(1), -s.ogs(1));
     const T gz = fma(z, s.idx(2), -s.ogs(2));
     int i = (int)gx, j = (int)gy, k = (int)gz;
-    i = i < 0 ? 0 : (i > a.nx - 1 ? a.nx - 1 : i);
-    j = j < 0 ? 0 : (j > a.ny - 1 ? a.ny - 1 : j);
-    k = k < 0 ? 0 : (k > a.nz - 1 ? a.nz - 1 : k);
+    // callers pass in-box positions: gx >= -ulp truncates to 0, only the upper
+    // face needs the clamp (kernels.py:541-552)
+    i = min(i, a.nx - 1);
+    j = min(j, a.ny - 1);
+    k = min(k, a.nz - 1);
     fx = gx - (T)i; fy = gy - (T)j; fz = gz - (T)k;
     return (i * a.NY + j) * a.NZ + k;
   }

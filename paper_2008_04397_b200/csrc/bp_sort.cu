@@ -50,6 +50,27 @@ __global__ void gather_perm(const T* __restrict__ src, const uint32_t* __restric
     dst[r] = src[order[r]];
 }
 
+// all eight particle arrays gathered through one read of the order: the
+// sorted copy lands in separate destination arrays (no copy back)
+template <typename T>
+__global__ void gather_perm8(const T* __restrict__ x, const T* __restrict__ y,
+                             const T* __restrict__ z, const T* __restrict__ u,
+                             const T* __restrict__ v, const T* __restrict__ w,
+                             const T* __restrict__ q, const long long* __restrict__ id,
+                             const uint32_t* __restrict__ order, T* __restrict__ ox,
+                             T* __restrict__ oy, T* __restrict__ oz, T* __restrict__ ou,
+                             T* __restrict__ ov, T* __restrict__ ow, T* __restrict__ oq,
+                             long long* __restrict__ oid, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const uint32_t j = __ldcs(order + r);
+    ox[r] = x[j]; oy[r] = y[j]; oz[r] = z[j];
+    ou[r] = u[j]; ov[r] = v[j]; ow[r] = w[j];
+    if (q) oq[r] = q[j];
+    if (id) oid[r] = id[j];
+  }
+}
+
 // fold one periodic axis of a (rows, NX, NY, NZ) grid: first += last; last = first
 __global__ void fold_axis(long long* a, int64_t rows, int NX, int NY, int NZ, int axis) {
   const int n1 = axis == 0 ? NY : NX;
@@ -210,6 +231,81 @@ int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, v
     if (!rc && ids) rc = permute_one<long long>(ids, i_out, tmp, n, s);
     if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
   }
+  if (rc) return rc;
+  return hbad ? 3 : 0;
+}
+
+// Sorted copy of src into dst (eight arrays each; q / ids optional), one
+// host synchronisation at the end.  On BP_ERR_DOMAIN dst is unspecified and
+// src untouched.
+int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* const* dst,
+                      int64_t* dst_ids, int64_t n, const double* origin, const double* spacing,
+                      const int64_t* counts, cudaStream_t s) {
+  if (n <= 0) return 0;
+  if (n > 0xffffffffLL) {
+    set_error("sort_by_cell: %lld particles exceed the 32-bit index space", (long long)n);
+    return -1;
+  }
+  const int64_t ncell = counts[0] * counts[1] * counts[2];
+  int end_bit = 1;
+  while (end_bit < 32 && (1LL << end_bit) < ncell) ++end_bit;
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, end_bit, s);
+  auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t nb = up((size_t)n * sizeof(uint32_t));
+  const size_t need = 4 * nb + up(sizeof(int)) + up((size_t)n * 8) + up(cub_bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_sort_mu);
+  SortWs& W = g_sort_ws[dev & 63];
+  if (W.bytes < need) {
+    if (W.base) {
+      cudaStreamSynchronize(s);
+      cudaFree(W.base);
+      W.base = nullptr;
+      W.bytes = 0;
+    }
+    int rc = check(cudaMalloc(&W.base, need), "sort workspace");
+    if (rc) return rc;
+    W.bytes = need;
+  }
+  char* p = static_cast<char*>(W.base);
+  uint32_t* k_in = (uint32_t*)p; p += nb;
+  uint32_t* k_out = (uint32_t*)p; p += nb;
+  uint32_t* i_in = (uint32_t*)p; p += nb;
+  uint32_t* i_out = (uint32_t*)p; p += nb;
+  int* bad = (int*)p; p += up(sizeof(int));
+  p += up((size_t)n * 8);
+  void* cub_tmp = p;
+  cudaMemsetAsync(bad, 0, sizeof(int), s);
+  int rc = keys_any(pbytes, src[0], src[1], src[2], n, origin, spacing, counts, k_in, nullptr,
+                    i_in, bad, s);
+  if (!rc)
+    rc = check(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k_in, k_out, i_in, i_out, n,
+                                               0, end_bit, s),
+               "radix sort");
+  if (!rc) {
+    if (pbytes == 8)
+      gather_perm8<double><<<blocks_for(n), 256, 0, s>>>(
+          (const double*)src[0], (const double*)src[1], (const double*)src[2],
+          (const double*)src[3], (const double*)src[4], (const double*)src[5],
+          (const double*)src[6], (const long long*)src_ids, i_out, (double*)dst[0],
+          (double*)dst[1], (double*)dst[2], (double*)dst[3], (double*)dst[4], (double*)dst[5],
+          (double*)dst[6], (long long*)dst_ids, n);
+    else
+      gather_perm8<float><<<blocks_for(n), 256, 0, s>>>(
+          (const float*)src[0], (const float*)src[1], (const float*)src[2],
+          (const float*)src[3], (const float*)src[4], (const float*)src[5],
+          (const float*)src[6], (const long long*)src_ids, i_out, (float*)dst[0],
+          (float*)dst[1], (float*)dst[2], (float*)dst[3], (float*)dst[4], (float*)dst[5],
+          (float*)dst[6], (long long*)dst_ids, n);
+    note_launch();
+    rc = check(cudaGetLastError(), "gather_perm8");
+  }
+  int hbad = 0;
+  if (!rc) rc = check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  if (!rc) rc = check(cudaStreamSynchronize(s), "sync");
   if (rc) return rc;
   return hbad ? 3 : 0;
 }

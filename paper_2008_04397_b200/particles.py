@@ -225,9 +225,43 @@ class DeviceParticles:
                    for a in ARRAYS + ("ids",))
 
     def sort_by_cell(self, geom, stream=None):
-        """On-device stable cell sort (bp_sort_by_cell): cell keys in f64 as
-        geometry.cell_index_of, stable radix sort, permutation of all eight
-        arrays in place."""
+        """On-device stable cell sort (bp_sort_by_cell_into): cell keys in f64
+        as geometry.cell_index_of, stable radix sort, one fused gather of all
+        eight arrays into a spare buffer set, which is then swapped in (the
+        spare is kept for the next sort)."""
+        import torch
+        from . import _lib
+        if self.n <= 1:
+            return self
+        L = _lib.load()
+        o = np.ascontiguousarray(geom.origin, np.float64)
+        d = np.ascontiguousarray(geom.spacings, np.float64)
+        c = np.ascontiguousarray(geom.counts, np.int64)
+        s = stream if stream is not None else torch.cuda.current_stream(self.x.device)
+        spare = getattr(self, "_spare", None)
+        if spare is None or spare[0].shape != self.x.shape:
+            spare = [torch.empty_like(a) for a in self.arrays()] + [torch.empty_like(self.ids)]
+        src = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in self.arrays()])
+        dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in spare[:7]])
+        rc = L.bp_sort_by_cell_into(self.x.element_size(), src,
+                                    ctypes.c_void_p(self.ids.data_ptr()), dst,
+                                    ctypes.c_void_p(spare[7].data_ptr()), self.n,
+                                    ctypes.c_void_p(o.ctypes.data), ctypes.c_void_p(d.ctypes.data),
+                                    ctypes.c_void_p(c.ctypes.data),
+                                    ctypes.c_void_p(s.cuda_stream))
+        _lib.check(rc, "sort_by_cell")
+        if rc == _lib.ERR_DOMAIN:
+            self._spare = spare
+            raise DomainError("positions below the box origin")
+        old = list(self.arrays()) + [self.ids]
+        for name, t in zip(ARRAYS + ("ids",), spare):
+            setattr(self, name, t)
+        self._spare = old
+        return self
+
+    def sort_by_cell_inplace(self, geom, stream=None):
+        """In-place variant (bp_sort_by_cell): no spare buffers, one scratch
+        array, eight gathers with copy back."""
         import torch
         from . import _lib
         if self.n <= 1:

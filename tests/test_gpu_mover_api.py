@@ -240,3 +240,32 @@ def test_device_sort_matches_reference_order(gpu):
     d2.sort_by_cell(geom2)
     assert np.array_equal(d2.ids.cpu().numpy(), order)
     assert np.array_equal(d2.u.cpu().numpy(), b2.u[order])
+
+
+def test_inplace_and_swap_sorts_agree(gpu):
+    """bp_sort_by_cell (in place) and bp_sort_by_cell_into (spare + swap)
+    produce the same order and bytes; a position below the origin raises
+    DomainError and leaves the buffer untouched."""
+    import torch
+    from paper_2008_04397_b200.errors import DomainError
+    from paper_2008_04397_b200.geometry import GridGeometry
+    from paper_2008_04397_b200.particles import DeviceParticles, ParticleBuffer
+    geom = GridGeometry.from_box((32, 16, 8), (6.4, 3.2, 1.6))
+    rng = np.random.default_rng(5)
+    n = 300_000
+    b = ParticleBuffer.empty(n, dtype=np.float32)
+    for a, L in zip("xyzuvw", geom.lengths + (1.0, 1.0, 1.0)):
+        getattr(b, a)[:] = (rng.random(n) * L).astype(np.float32)
+    b.q_p[:] = rng.random(n).astype(np.float32)
+    d1 = DeviceParticles.from_host(b, torch.device("cuda")).sort_by_cell(geom)
+    d2 = DeviceParticles.from_host(b, torch.device("cuda")).sort_by_cell_inplace(geom)
+    for a in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
+        assert torch.equal(getattr(d1, a), getattr(d2, a)), a
+    d1.sort_by_cell(geom)  # second sort reuses the spare set: already sorted -> same
+    assert torch.equal(d1.ids, d2.ids)
+    b.x[7] = -1.0
+    d3 = DeviceParticles.from_host(b, torch.device("cuda"))
+    before = d3.ids.clone()
+    with pytest.raises(DomainError):
+        d3.sort_by_cell(geom)
+    assert torch.equal(d3.ids, before)
