@@ -145,7 +145,8 @@ class DeviceSimulation:
 
     # ------------------------------------------------------------ phases
     def set_fields(self, E=None, B=None):
-        """Phase 1: host E/B (numpy, rank 0) -> HBM, broadcast to all ranks."""
+        """Phase 1: host E/B (numpy, rank 0) -> HBM, broadcast to all ranks
+        (collective: all ranks call it; only rank 0's arrays are used)."""
         if E is not None:
             self.E.copy_(self.torch.from_numpy(np.ascontiguousarray(E)), non_blocking=False)
         if B is not None:
@@ -192,6 +193,11 @@ class DeviceSimulation:
         for w in works:
             w.wait()
         ev[3].record(s)
+        if self.distributed:
+            # every rank raises together (a one-sided raise would strand the
+            # others in the next collective)
+            import torch.distributed as dist
+            dist.all_reduce(self.status, op=dist.ReduceOp.MAX, group=self.group)
         ev[3].synchronize()
         st = int(self.status.item())
         if st == _lib.ERR_RUNAWAY:
@@ -223,9 +229,12 @@ class DeviceSimulation:
 
     def run_cycle(self, E=None, B=None):
         """One cycle on device: phases 1-4 and (when due) 6.  The host solve
-        (phase 5) is the caller's; moments for it are in ``self.acc``."""
+        (phase 5) is the caller's; moments for it are in ``self.acc``.
+
+        Distributed: every rank calls this collectively; rank 0 passes the new
+        E/B (others may pass None) and the broadcast runs on all ranks."""
         torch = self.torch
-        if E is not None or B is not None:
+        if E is not None or B is not None or self.distributed:
             self.set_fields(E, B)
         p3, kt = self.phase3()
         self.fold_moments()
