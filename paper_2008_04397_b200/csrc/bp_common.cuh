@@ -223,14 +223,22 @@ struct Slot {
   u64 s0, s1, s2;
 };
 
+__device__ __forceinline__ void red_add_always(i64* p, i64 v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+// Flush a slot: one REDG.ADD.64 per value, issued unconditionally (a zero
+// add is cheaper than the branch around it); lanes of groups 2-3 own only
+// two values.
 __device__ __forceinline__ void slot_flush(const Slot& sl, i64* __restrict__ acc, int NN,
                                            int m0, int coff, bool third) {
   if (sl.key < 0) return;
   const u64 bias = (u64)sl.n * (u64)kMagicBits;
-  i64* p = acc + (size_t)m0 * NN + sl.key + coff;
-  red_add(p, (i64)(sl.s0 - bias));
-  red_add(p + (size_t)4 * NN, (i64)(sl.s1 - bias));
-  if (third) red_add(p + (size_t)8 * NN, (i64)(sl.s2 - bias));
+  i64* p = acc + ((size_t)m0 * NN + (size_t)(sl.key + coff));
+  const size_t st4 = (size_t)4 * NN;
+  red_add_always(p, (i64)(sl.s0 - bias));
+  red_add_always(p + st4, (i64)(sl.s1 - bias));
+  if (third) red_add_always(p + 2 * st4, (i64)(sl.s2 - bias));
 }
 
 // quantised value as a biased bit pattern: bits(M) + rint(t)

@@ -23,7 +23,14 @@ def stats(step):
         t = key[:n].view(-1, 32)
         mode = torch.mode(t, dim=1).values
         nonmaj = (t != mode[:, None]).sum(1).double()
-        print(f"step {step} species {sid}: mean non-majority per tile {nonmaj.mean():.2f}, "
+        srt = torch.sort(t, dim=1).values
+        distinct = 1 + (srt[:, 1:] != srt[:, :-1]).sum(1).double()
+        # distinct stray cells across a window of 4 consecutive tiles of a warp
+        w4 = t[: t.shape[0] // 4 * 4].view(-1, 128)
+        s4 = torch.sort(w4, dim=1).values
+        d4 = 1 + (s4[:, 1:] != s4[:, :-1]).sum(1).double()
+        print(f"step {step} species {sid}: non-majority/tile {nonmaj.mean():.2f}, "
+              f"distinct cells/tile {distinct.mean():.2f}, distinct cells/4 tiles {d4.mean():.2f}, "
               f"uniform tiles {(nonmaj == 0).double().mean():.3f}", flush=True)
 stats(0)
 for s in range(1, 11):
