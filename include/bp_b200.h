@@ -152,6 +152,20 @@ int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int
                  const double* origin, const double* spacing, const int64_t* counts,
                  int64_t* keys, void* stream);
 
+/* Exact int64 sum over species of n-element grids (fields.total_moments,
+ * fields.py:170-179): total[i] = sum_s accs[s][i].  Device pointers. */
+int bp_moments_total(const int64_t* const* accs, int nspecies, int64_t n, int64_t* total,
+                     void* stream);
+
+/* Scalar implicit plasma response (maxwell.plasma_susceptibility,
+ * maxwell.py:163-179), bitwise: chi[i] = (0.5 theta dt^2) *
+ * max(0, sum_s (4 pi rho_s[i]) qom_s) with rho_s = acc_s * 2^-43 (rounded to
+ * f32 and back when single != 0).  rho_rows[s] = row 0 of species s's
+ * accumulator (device); qom is a host array. */
+int bp_susceptibility(const int64_t* const* rho_rows, const double* qom, int nspecies,
+                      int single, double theta, double dt, int64_t n, double* chi,
+                      void* stream);
+
 /* Exact merge of duplicated periodic node planes of a (rows, nx+1, ny+1,
  * nz+1) int64 grid (fields.fold_periodic, fields.py:28-47). */
 int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void* stream);

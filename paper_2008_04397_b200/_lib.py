@@ -27,7 +27,7 @@ EXPORTS = (
     "bp_version", "bp_last_error", "bp_kernel_launches", "bp_fused_span", "bp_push_span",
     "bp_deposit_span", "bp_gather_span", "bp_fused_span_ex",
     "bp_fused_span_host", "bp_sort_by_cell", "bp_sort_by_cell_into", "bp_cell_keys",
-    "bp_fold_periodic_i64",
+    "bp_fold_periodic_i64", "bp_moments_total", "bp_susceptibility",
 )
 
 _P = ctypes.c_void_p
@@ -57,6 +57,8 @@ _SIGS = {
     "bp_sort_by_cell_into": (_INT, [_INT, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "bp_cell_keys": (_INT, [_INT, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "bp_fold_periodic_i64": (_INT, [_P, _I64, _P, _P]),
+    "bp_moments_total": (_INT, [_P, _INT, _I64, _P, _P]),
+    "bp_susceptibility": (_INT, [_P, _P, _INT, _INT, _D, _D, _I64, _P, _P]),
 }
 
 _lib = None

@@ -54,6 +54,10 @@ int fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, cudaStre
 int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* const* dst,
                       int64_t* dst_ids, int64_t n, const double* origin, const double* spacing,
                       const int64_t* counts, cudaStream_t s);
+int moments_total(const long long* const* rows, int ns, int64_t n, long long* total,
+                  cudaStream_t st);
+int susceptibility(const long long* const* rho_rows, const double* qom, int ns, int single,
+                   double factor, int64_t n, double* chi, cudaStream_t st);
 
 namespace {
 
@@ -464,6 +468,30 @@ int bp_cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int
                  int64_t* keys, void* stream) {
   ensure_pool();
   return cell_keys(pbytes, xs, ys, zs, n, origin, spacing, counts, keys, (cudaStream_t)stream);
+}
+
+int bp_moments_total(const int64_t* const* accs, int nspecies, int64_t n, int64_t* total,
+                     void* stream) {
+  if (!accs || !total || n < 0) {
+    set_error("bp_moments_total: null arrays or negative size");
+    return BP_EINVAL;
+  }
+  if (n == 0) return BP_OK;
+  return moments_total(reinterpret_cast<const long long* const*>(accs), nspecies, n,
+                       reinterpret_cast<long long*>(total), (cudaStream_t)stream);
+}
+
+int bp_susceptibility(const int64_t* const* rho_rows, const double* qom, int nspecies,
+                      int single, double theta, double dt, int64_t n, double* chi,
+                      void* stream) {
+  if (!rho_rows || !qom || !chi || n < 0) {
+    set_error("bp_susceptibility: null arrays or negative size");
+    return BP_EINVAL;
+  }
+  if (n == 0) return BP_OK;
+  const double factor = 0.5 * theta * dt * dt;  // maxwell.py:178, left to right
+  return susceptibility(reinterpret_cast<const long long* const*>(rho_rows), qom, nspecies,
+                        single, factor, n, chi, (cudaStream_t)stream);
 }
 
 int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void* stream) {

@@ -187,6 +187,56 @@ def init_maxwellian(species, geom, density_fn=None, seed=1, precision=None, drif
     return buf.validate(geom)
 
 
+# ------------------------------------------------------------ checkpoint
+
+CHECKPOINT_MAGIC = b"BPIC"
+CHECKPOINT_VERSION = 1
+CHECKPOINT_VERSION_FULL = 2
+_HEADER = "<4sIQB"
+
+
+def write_particles(buf, path, version=CHECKPOINT_VERSION):
+    """Particle checkpoint.  Version 1 is the reference format byte for byte
+    (particles.py:244-255: little-endian ``<4sIQB`` header — magic, version,
+    count, item size — then x y z u v w).  Version 2 appends q_p (same item
+    size), the int64 ids and the species id, so a run can resume deposition
+    (the reference's v1 drops them)."""
+    import struct
+    item = buf.dtype.itemsize
+    with open(path, "wb") as fh:
+        fh.write(struct.pack(_HEADER, CHECKPOINT_MAGIC, version, buf.n, item))
+        for arr in buf.components():
+            fh.write(np.ascontiguousarray(arr, dtype=f"<f{item}").tobytes())
+        if version >= CHECKPOINT_VERSION_FULL:
+            fh.write(np.ascontiguousarray(buf.q_p, dtype=f"<f{item}").tobytes())
+            fh.write(np.ascontiguousarray(buf.ids, dtype="<i8").tobytes())
+            fh.write(struct.pack("<q", int(buf.species_id)))
+
+
+def read_particles(path, species_id=0):
+    """Read a v1 (reference: q_p zero-filled, fresh ids, particles.py:258-274)
+    or v2 checkpoint."""
+    import struct
+    with open(path, "rb") as fh:
+        raw = fh.read(struct.calcsize(_HEADER))
+        magic, version, n, item = struct.unpack(_HEADER, raw)
+        if magic != CHECKPOINT_MAGIC:
+            raise IntegrityError(f"bad checkpoint magic {magic!r}")
+        if version not in (CHECKPOINT_VERSION, CHECKPOINT_VERSION_FULL):
+            raise IntegrityError(f"unsupported checkpoint version {version}")
+        dt = np.float32 if item == 4 else np.float64
+        comps = [np.frombuffer(fh.read(n * item), dtype=f"<f{item}").astype(dt)
+                 for _ in range(6)]
+        if version >= CHECKPOINT_VERSION_FULL:
+            q = np.frombuffer(fh.read(n * item), dtype=f"<f{item}").astype(dt)
+            ids = np.frombuffer(fh.read(n * 8), dtype="<i8").astype(np.int64)
+            species_id = struct.unpack("<q", fh.read(8))[0]
+        else:
+            q = np.zeros(n, dt)
+            ids = np.arange(n, dtype=np.int64)
+    return ParticleBuffer(*comps, q_p=q, ids=ids, species_id=species_id)
+
+
 # ------------------------------------------------------- device residency
 
 class DeviceParticles:

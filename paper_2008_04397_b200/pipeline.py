@@ -222,6 +222,35 @@ class DeviceSimulation:
     def moments_host(self):
         return [a.cpu().numpy() for a in self.acc]
 
+    def total_moments(self):
+        """Exact int64 sum of the species grids on device (fields.total_moments)."""
+        torch = self.torch
+        L = _lib.load()
+        total = torch.empty_like(self.acc[0])
+        rows = (ctypes.c_void_p * len(self.acc))(*[a.data_ptr() for a in self.acc])
+        s = torch.cuda.current_stream(self.device)
+        _lib.check(L.bp_moments_total(rows, len(self.acc), total.numel(),
+                                      ctypes.c_void_p(total.data_ptr()),
+                                      ctypes.c_void_p(s.cuda_stream)), "moments_total")
+        return total
+
+    def susceptibility(self, theta):
+        """maxwell.plasma_susceptibility of the current (folded) moments,
+        computed on device (bitwise the reference); returns a float64 device
+        tensor of node shape."""
+        torch = self.torch
+        L = _lib.load()
+        chi = torch.empty(self.geom.node_shape, dtype=torch.float64, device=self.device)
+        rows = (ctypes.c_void_p * len(self.acc))(*[a.data_ptr() for a in self.acc])
+        qom = np.ascontiguousarray([s.qom for s in self.species], np.float64)
+        s = torch.cuda.current_stream(self.device)
+        single = 1 if self.precision.fields == "single" else 0
+        _lib.check(L.bp_susceptibility(rows, ctypes.c_void_p(qom.ctypes.data), len(self.acc),
+                                       single, float(theta), float(self.dt), chi.numel(),
+                                       ctypes.c_void_p(chi.data_ptr()),
+                                       ctypes.c_void_p(s.cuda_stream)), "susceptibility")
+        return chi
+
     def sort(self):
         for p in self.particles:
             if p is not None:

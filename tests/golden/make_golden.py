@@ -37,7 +37,8 @@ from batchpic.config import InitConfig, PrecisionMode, SimulationDeck, SpeciesPa
 from batchpic.diagnostics import energy_ledger
 from batchpic.fields import MOMENT_SCALE
 from batchpic.geometry import GridGeometry
-from batchpic.particles import sort_by_cell, ParticleBuffer
+from batchpic.maxwell import plasma_susceptibility
+from batchpic.particles import sort_by_cell, ParticleBuffer, write_particles
 from batchpic.pipeline import make_state, run_cycle
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -133,6 +134,26 @@ def sort_case():
     np.savez_compressed(os.path.join(OUT, "sort.npz"), **rec)
 
 
+def checkpoint_case():
+    """Bytes of the reference's BPIC v1 checkpoint (particles.py:244-274)."""
+    import tempfile
+    rec = {}
+    rng = np.random.default_rng(12)
+    for dt in (np.float64, np.float32):
+        buf = ParticleBuffer.empty(37, dtype=dt)
+        for nm in ("x", "y", "z", "u", "v", "w", "q_p"):
+            getattr(buf, nm)[:] = rng.random(37).astype(dt)
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "p.bin")
+            write_particles(buf, path)
+            raw = open(path, "rb").read()
+        tag = np.dtype(dt).name
+        rec[f"bytes_{tag}"] = np.frombuffer(raw, np.uint8)
+        for nm in ("x", "y", "z", "u", "v", "w", "q_p"):
+            rec[f"{tag}_{nm}"] = getattr(buf, nm)
+    np.savez_compressed(os.path.join(OUT, "checkpoint.npz"), **rec)
+
+
 def c1_deck(mode, cycles):
     pd = {"double": ("double", "double"), "single": ("single", "single"),
           "mixed": ("single", "double")}[mode]
@@ -179,6 +200,12 @@ def c1_case(mode, cycles=10, stride=64):
         rec["E_final"] = state.fields.E.copy()
         rec["B_final"] = state.fields.B.copy()
         rec["ledger"] = np.array(led)
+        # phase-4/5 consumer of the moments: the susceptibility the host solve
+        # used for the last cycle (maxwell.py:163-179)
+        rec["chi_last"] = plasma_susceptibility(
+            [state.moments[s] for s in sorted(state.moments)], deck.species, deck.dt,
+            deck.theta, state.geom)
+        rec["theta"] = deck.theta
         for s, buf in enumerate(state.buffers):
             rec[f"acc_{s}"] = state.moments[s].acc.copy()  # folded (phase 4)
             for nm in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
@@ -194,6 +221,7 @@ def main():
     for mode in MODES:
         kernel_cases(mode)
     sort_case()
+    checkpoint_case()
     for mode in MODES:
         c1_case(mode)
     for f in sorted(os.listdir(OUT)):

@@ -38,12 +38,14 @@ def _run(mode, arith):
         Bf = g["B"][c + 1] if c + 1 < int(g["cycles"]) else g["B_final"]
         ledger.append([field_energy(Ef, Bf, geom)] + sim.kinetic_energy())
     parts = [p.to_host() for p in sim.particles]
-    return g, parts, sim.moments_host(), np.array(ledger)
+    sim.chi = sim.susceptibility(float(g["theta"])).cpu().numpy()
+    sim.total = sim.total_moments().cpu().numpy()
+    return g, parts, sim.moments_host(), np.array(ledger), sim
 
 
 @pytest.mark.parametrize("mode", list(MODES))
 def test_c1_replay_parity_bitwise(gpu, mode):
-    g, parts, accs, ledger = _run(mode, "parity")
+    g, parts, accs, ledger, sim = _run(mode, "parity")
     for s, buf in enumerate(parts):
         for nm in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
             sha = hashlib.sha256(np.ascontiguousarray(getattr(buf, nm)).tobytes()).hexdigest()
@@ -52,11 +54,14 @@ def test_c1_replay_parity_bitwise(gpu, mode):
     # kinetic terms are f64 sums in a different order than numpy's: compare to
     # a few ulps; the field term is the same formula on the same arrays
     assert np.allclose(ledger, g["ledger"], rtol=1e-13, atol=0)
+    # device phase 4: exact species total and the host solve's susceptibility
+    assert np.array_equal(sim.total, sum(g[f"acc_{s}"] for s in range(4)))
+    assert np.array_equal(sim.chi, g["chi_last"])
 
 
 @pytest.mark.parametrize("mode", list(MODES))
 def test_c1_replay_fast_within_tolerance(gpu, mode):
-    g, parts, accs, ledger = _run(mode, "fast")
+    g, parts, accs, ledger, sim = _run(mode, "fast")
     rtol = 1e-10 if mode == "double" else 1e-4
     # chaotic orbits amplify round-off over 10 cycles; SURVEY.md §8c measured a
     # 1-ulp perturbation growing to 1.6e-14 (f64) / 2.7e-6 (f32) of the max

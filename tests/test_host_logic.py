@@ -77,3 +77,39 @@ def test_product_path_refuses_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(_lib.BackendError):
         _lib.load()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_checkpoint_v1_is_the_reference_format(tmp_path, dtype):
+    """write_particles(version=1) reproduces the reference's file byte for
+    byte; read_particles reads the reference's file (q_p zero, fresh ids)."""
+    from paper_2008_04397_b200.particles import ParticleBuffer, read_particles, write_particles
+    g = golden("checkpoint.npz")
+    n = g[f"{dtype}_x"].shape[0]
+    buf = ParticleBuffer.empty(n, dtype=np.dtype(dtype).type)
+    for nm in ("x", "y", "z", "u", "v", "w", "q_p"):
+        getattr(buf, nm)[:] = g[f"{dtype}_{nm}"]
+    path = tmp_path / "p.bin"
+    write_particles(buf, path)
+    assert path.read_bytes() == g[f"bytes_{dtype}"].tobytes()
+    ref = tmp_path / "ref.bin"
+    ref.write_bytes(g[f"bytes_{dtype}"].tobytes())
+    back = read_particles(ref)
+    assert back.dtype == np.dtype(dtype)
+    for nm in ("x", "y", "z", "u", "v", "w"):
+        assert np.array_equal(getattr(back, nm), getattr(buf, nm))
+    assert (back.q_p == 0).all() and np.array_equal(back.ids, np.arange(n))
+
+
+def test_checkpoint_v2_keeps_charge_and_ids(tmp_path):
+    from paper_2008_04397_b200.particles import ParticleBuffer, read_particles, write_particles
+    rng = np.random.default_rng(3)
+    buf = ParticleBuffer.empty(100, species_id=2, dtype=np.float32)
+    for nm in ("x", "y", "z", "u", "v", "w", "q_p"):
+        getattr(buf, nm)[:] = rng.random(100).astype(np.float32)
+    buf.ids[:] = rng.permutation(100)
+    write_particles(buf, tmp_path / "p2.bin", version=2)
+    back = read_particles(tmp_path / "p2.bin")
+    assert back.species_id == 2
+    for nm in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
+        assert np.array_equal(getattr(back, nm), getattr(buf, nm)), nm
