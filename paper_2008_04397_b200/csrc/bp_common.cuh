@@ -80,7 +80,12 @@ struct SpanParams {
   // every full 32-particle tile of the span is 16-byte aligned in all arrays:
   // tiles stream through shared memory with TMA bulk copies
   int bulk;
+  // dynamic work distribution: next unclaimed particle of the span
+  unsigned long long* work;
 };
+
+// particles per dynamically claimed chunk (32 tiles of a warp)
+constexpr int kChunk = 1024;
 
 // ---- TMA bulk copies and mbarriers (sm_90+ PTX, UBLKCP in SASS) ----------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -416,11 +421,6 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
   extern __shared__ double stage_all[];
   const unsigned lane = lane_id();
   const int wib = threadIdx.x >> 5;
-  const i64 nwarps = (i64)gridDim.x * (blockDim.x >> 5);
-  const i64 gw = (i64)blockIdx.x * (blockDim.x >> 5) + wib;
-  const i64 per = ((a.count + nwarps - 1) / nwarps + 31) & ~(i64)31;
-  const i64 w0 = gw * per;
-  const i64 w1 = w0 + per < a.count ? w0 + per : a.count;
   // per-warp shared memory: deposit staging [+ particle tile stages when bulk]
   double* const st_bs =
       stage_all + (size_t)wib * (a.bulk ? warp_smem_doubles<P>() : kWarpStage);
@@ -451,6 +451,16 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
     fence_proxy_async();
   }
   __syncwarp();
+  unsigned phase = 0;  // bit s: parity of stage s's next completion
+  // Warps claim contiguous chunks of the span from a global counter (no tail
+  // of idle SMs, no imbalance from uneven disorder); slot sums persist across
+  // chunks — any grouping of the integer sums is exact.
+  for (;;) {
+  i64 w0 = 0;
+  if (lane == 0) w0 = (i64)atomicAdd(a.work, (unsigned long long)kChunk);
+  w0 = __shfl_sync(0xffffffffu, w0, 0);
+  if (w0 >= a.count) break;
+  const i64 w1 = w0 + kChunk < a.count ? w0 + kChunk : a.count;
   auto full = [&](i64 t) { return a.bulk && t + 32 <= w1; };
   auto issue = [&](i64 t, int stg) {
     if (lane == 0) {
@@ -459,8 +469,12 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
         bulk_load(tiles + (stg * 7 + k) * 32, arr[k] + a.start + t, tile_bytes, bars + stg);
     }
   };
-  if (w0 < w1 && full(w0)) issue(w0, 0);
-  unsigned phase = 0;  // bit s: parity of stage s's next completion
+  if (full(w0)) {
+    // stage 0 may still feed the previous chunk's last bulk store
+    if (DO_PUSH && lane == 0) bulk_wait_read_all();
+    __syncwarp();
+    issue(w0, 0);
+  }
   int it = 0;
   for (i64 t0 = w0; t0 < w1; t0 += 32, ++it) {
     const int stg = it & 1;
@@ -525,6 +539,7 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
       __syncwarp();
     }
   }
+  }  // chunks
   if (DO_DEPOSIT) {
     slot_flush(A, a.acc, a.NN, lg, coff, third);
     slot_flush(Bs, a.acc, a.NN, lg, coff, third);

@@ -56,6 +56,7 @@ SpanParams<P, F> make_params(const Call& c) {
   a.d.beta = (double)a.beta; a.d.one = (double)a.one; a.d.two = (double)a.two;
   a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
   a.iv_max = nullptr;
+  a.work = nullptr;
   {
     // TMA bulk tiles need every full tile 16-byte aligned in all 7 arrays
     const void* ptrs[7] = {c.x, c.y, c.z, c.u, c.v, c.w, c.q};
@@ -152,7 +153,8 @@ int run_span(const Call& c, bool prescale_ok, cudaStream_t s) {
     return -2;
   }
   unsigned long long* ivm = reinterpret_cast<unsigned long long*>((char*)fn + rec_bytes);
-  cudaMemsetAsync(ivm, 0, sizeof(unsigned long long), s);
+  cudaMemsetAsync(ivm, 0, 2 * sizeof(unsigned long long), s);  // iv_max, work counter
+  a.work = ivm + 1;
   const int pb = (a.NN + 255) / 256 < 4096 ? (a.NN + 255) / 256 : 4096;
   pack_nodes<F, T><<<pb, 256, 0, s>>>(PUSH ? a.E : nullptr, PUSH ? a.B : nullptr,
                                       DEP ? a.invvol : nullptr, a.NN, fn, ivm);
