@@ -144,6 +144,17 @@ __device__ __forceinline__ unsigned lane_id() {
   return r;
 }
 
+// one node record as 16-byte vector stores
+__device__ __forceinline__ void store_record(float* o, const float* r) {
+  reinterpret_cast<float4*>(o)[0] = make_float4(r[0], r[1], r[2], r[3]);
+  reinterpret_cast<float4*>(o)[1] = make_float4(r[4], r[5], r[6], r[7]);
+}
+__device__ __forceinline__ void store_record(double* o, const double* r) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    reinterpret_cast<double2*>(o)[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
+
 // E, B, invvol -> one 8-element record per node, so one corner of a gather is
 // a couple of 16-byte loads from one record and the deposit's control volume
 // comes from the same line.  T = double (parity: exact widening) or the fast
@@ -165,11 +176,18 @@ __global__ void pack_nodes(const F* __restrict__ E, const F* __restrict__ B,
     r[5] = B ? (T)B[2 * NN + n] : T(0);
     r[6] = invvol ? (T)invvol[n] : T(0);
     r[7] = T(0);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) out[(size_t)n * 8 + k] = r[k];
+    store_record(out + (size_t)n * 8, r);
   }
-  // non-negative doubles order like their bit patterns
-  if (iv_max && vmax > 0.0) atomicMax(iv_max, (unsigned long long)__double_as_longlong(vmax));
+  // one same-address atomic per warp, not per thread (a per-thread atomicMax
+  // serialised ~NN updates in one L2 slice); non-negative doubles order like
+  // their bit patterns
+  unsigned long long bits = (unsigned long long)__double_as_longlong(vmax);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = b > bits ? b : bits;
+  }
+  if (iv_max && bits != 0ull && (threadIdx.x & 31) == 0) atomicMax(iv_max, bits);
 }
 
 // --------------------------------------------------------------------------
