@@ -144,6 +144,20 @@ __device__ __forceinline__ unsigned lane_id() {
   return r;
 }
 
+// 32-byte read-only loads (LDG.E.ENL2.256, sm_100+): one node record of
+// floats, or half a record of doubles, per instruction
+__device__ __forceinline__ void ldg256(const float* p, float r[8]) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ldg256(const double* p, double r[4]) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+      : "l"(p));
+}
+
 // one node record as 16-byte vector stores
 __device__ __forceinline__ void store_record(float* o, const float* r) {
   reinterpret_cast<float4*>(o)[0] = make_float4(r[0], r[1], r[2], r[3]);
@@ -293,7 +307,7 @@ __device__ __forceinline__ void fold_one(Slot& S, const double* st_bs, const dou
 // 3-input 64-bit add (IADD3 + IADD3.X).
 template <bool PRESCALE, bool MAGIC, bool FMA>
 __device__ __forceinline__ void fold_tile(Slot& S, const double* st_bs, const double* st_mv,
-                                          int lc, int lg, double sc) {
+                                          int lc, int lg, bool third, double sc) {
   const double* br = st_bs + lc * kRow;
   const double* mr = st_mv + lg * 3 * kRow;
 #pragma unroll 4
@@ -301,10 +315,13 @@ __device__ __forceinline__ void fold_tile(Slot& S, const double* st_bs, const do
     const double2 b = *reinterpret_cast<const double2*>(br + k);
     const double2 m0 = *reinterpret_cast<const double2*>(mr + k);
     const double2 m1 = *reinterpret_cast<const double2*>(mr + kRow + k);
-    const double2 m2 = *reinterpret_cast<const double2*>(mr + 2 * kRow + k);
     S.s0 += qbits<PRESCALE, MAGIC, FMA>(b.x, m0.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m0.y, sc);
     S.s1 += qbits<PRESCALE, MAGIC, FMA>(b.x, m1.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m1.y, sc);
-    S.s2 += qbits<PRESCALE, MAGIC, FMA>(b.x, m2.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m2.y, sc);
+    if (third) {
+      // lane groups 2-3 own two values: their third row is not read
+      const double2 m2 = *reinterpret_cast<const double2*>(mr + 2 * kRow + k);
+      S.s2 += qbits<PRESCALE, MAGIC, FMA>(b.x, m2.x, sc) + qbits<PRESCALE, MAGIC, FMA>(b.y, m2.y, sc);
+    }
   }
   S.n += 32;
 }
@@ -411,9 +428,9 @@ __device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict_
     __syncwarp();
   }
   if (magic)
-    fold_tile<PRESCALE, true, FMA>(A, st_bs, st_mv, lc, lg, sc);
+    fold_tile<PRESCALE, true, FMA>(A, st_bs, st_mv, lc, lg, third, sc);
   else
-    fold_tile<PRESCALE, false, FMA>(A, st_bs, st_mv, lc, lg, sc);
+    fold_tile<PRESCALE, false, FMA>(A, st_bs, st_mv, lc, lg, third, sc);
 }
 
 // --------------------------------------------------------------------------

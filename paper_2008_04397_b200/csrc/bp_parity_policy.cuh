@@ -63,8 +63,11 @@ __device__ __forceinline__ void gather_records(const double* __restrict__ fn, in
   const int off[8] = {0, sx, sy, sx + sy, 1, sx + 1, sy + 1, sx + sy + 1};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const double2* r = reinterpret_cast<const double2*>(fn + (size_t)(n000 + off[k]) * 8);
-    const double2 a0 = __ldg(r), a1 = __ldg(r + 1), a2 = __ldg(r + 2);
+    const double* rec = fn + (size_t)(n000 + off[k]) * 8;
+    double q4[4];
+    ldg256(rec, q4);
+    const double2 a0 = make_double2(q4[0], q4[1]), a1 = make_double2(q4[2], q4[3]);
+    const double2 a2 = __ldg(reinterpret_cast<const double2*>(rec) + 2);
     if (k == 0) {
       s[0] = w[0] * a0.x; s[1] = w[0] * a0.y; s[2] = w[0] * a1.x;
       s[3] = w[0] * a1.y; s[4] = w[0] * a2.x; s[5] = w[0] * a2.y;
