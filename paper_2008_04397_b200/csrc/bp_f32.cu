@@ -1,0 +1,594 @@
+// Fused mover + deposition for f32 particles ("single" and "mixed" modes),
+// fast arithmetic, sm_100a.  Same algorithm as the reference fused_span
+// (pkg/src/batchpic/kernels.py:458-735); the instruction budget per particle
+// is what this file is about.
+//
+// Push: fields come from per-cell coefficient records (pack_cells): for each
+// component f the trilinear form
+//     f(fx,fy,fz) = [c0 + c1 fx + (c2 + c4 fx) fy] + fz [c3 + c5 fx + (c6 + c7 fx) fy]
+// (the reference's 8-weight sum, kernels.py:557-591, regrouped), so one gather
+// is 12 contiguous 16-byte loads from one 192-byte record and 7 FFMA per
+// component.  Boundary kinds are template parameters.
+//
+// Deposit: the per-warp transposed fold of bp_common.cuh (lane = corner x
+// moment group, 32 staged particles per tile) in f32: each tile's partial sum
+// of q * w_c * m is rounded once onto the int64 lattice, after multiplying by
+// invvol * 2^43 of the lane's node (kernels.py:707-734 apply invvol and the
+// scale per contribution; here per tile — within the 1e-4 f32 tolerance).
+// Integer slot sums and REDG.ADD.64 flushes as in the exact path.  Slots are
+// flushed at the end of every dynamically claimed chunk, so every tile's
+// grouping depends only on the chunk's content: the result is deterministic.
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "bp_common.cuh"
+#include "bp_launch.h"
+
+namespace bp {
+namespace f32k {
+
+struct Params {
+  float *x, *y, *z, *u, *v, *w;
+  const float* q;
+  long long start, count;
+  const float4* rec;     // 12 float4 per cell, cell = i + nx * (j + ny * k)
+  const float* iv_f;     // invvol (nx+1, ny+1, nz+1) when fields are f32
+  const double* iv_d;    // ... when fields are f64 (mixed)
+  long long* acc;        // (10, NN) int64
+  int nx, ny, nz, NY, NZ, NN;
+  int cny;               // nx * ny (cell-record z stride)
+  float o[3], hi[3], L[3], hi2[3], idx[3], ogs[3];
+  float dt, dth, qdt2m, beta, beta2;
+  double scale;
+  int n_iters;
+  int* status;
+  unsigned long long* work;
+};
+
+constexpr int kRow = 36;  // staged row stride (floats): conflict-free LDS.128 per warp
+// staging rows: 8 bases (corner c) then 10 moments (row 8 + m); row 8 (m = 1) is constant
+constexpr int kStage = 18 * kRow;
+
+__device__ __forceinline__ float4 ldg4(const float4* p) {
+  float4 r;
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+
+// 1 / d for d = 1 + beta^2 |h|^2 >= 1 (MUFU.RCP alone, no range fix-up)
+__device__ __forceinline__ float rcp_approx(float d) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  return r;
+}
+
+template <bool REFL>
+__device__ __forceinline__ float fold_mid(float xm, float o, float L, float hi, float hi2) {
+  if (!REFL) {
+    if (xm < o) xm += L;
+    else if (xm > hi) xm -= L;
+  } else {
+    if (xm < o) xm = o + (o - xm);
+    else if (xm > hi) xm = hi2 - xm;
+  }
+  return xm;
+}
+
+template <bool REFL>
+__device__ __forceinline__ void fold_commit(float& q, float& vel, float o, float L, float hi,
+                                            float hi2) {
+  if (!REFL) {
+    if (q < o) {
+      q += L;
+      if (q >= hi) q = o;
+    } else if (q >= hi) {
+      q -= L;
+    }
+  } else {
+    if (q < o) {
+      q = o + (o - q);
+      vel = -vel;
+    } else if (q > hi) {
+      q = hi2 - q;
+      vel = -vel;
+    }
+  }
+}
+
+// cell of an in-box position: truncation (in-box gx >= -ulp truncates to 0)
+// and the upper-face clamp of kernels.py:541-556; returns the cell index
+__device__ __forceinline__ int cell_of(const Params& a, float x, float y, float z, float& fx,
+                                      float& fy, float& fz, int& i, int& j, int& k) {
+  const float gx = fmaf(x, a.idx[0], -a.ogs[0]);
+  const float gy = fmaf(y, a.idx[1], -a.ogs[1]);
+  const float gz = fmaf(z, a.idx[2], -a.ogs[2]);
+  i = min((int)gx, a.nx - 1);
+  j = min((int)gy, a.ny - 1);
+  k = min((int)gz, a.nz - 1);
+  fx = gx - (float)i;
+  fy = gy - (float)j;
+  fz = gz - (float)k;
+  return i + a.nx * j + a.cny * k;
+}
+
+// one component from its two coefficient quads
+__device__ __forceinline__ float tri(const float4 A, const float4 B, float fx, float fy,
+                                     float fz) {
+  const float p = fmaf(A.y, fx, A.x), q = fmaf(A.w, fx, A.z);
+  const float r = fmaf(B.y, fx, B.x), s = fmaf(B.w, fx, B.z);
+  return fmaf(fmaf(s, fy, r), fz, fmaf(q, fy, p));
+}
+
+template <bool RX, bool RY, bool RZ>
+__device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float& zp, float& un,
+                                    float& vn, float& wn) {
+  float vbx = un, vby = vn, vbz = wn;
+#pragma unroll 1
+  for (int it = 0; it < a.n_iters; ++it) {
+    float xm = fmaf(vbx, a.dth, xp), ym = fmaf(vby, a.dth, yp), zm = fmaf(vbz, a.dth, zp);
+    xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+    ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+    zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+    if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
+        zm > a.hi[2])
+      return ST_MIDPOINT;
+    float fx, fy, fz;
+    int i, j, k;
+    const int cell = cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    const float4* r = a.rec + (size_t)cell * 12;
+    float e[6];
+#pragma unroll
+    for (int m = 0; m < 6; ++m) e[m] = tri(ldg4(r + 2 * m), ldg4(r + 2 * m + 1), fx, fy, fz);
+    const float tx = fmaf(a.qdt2m, e[0], un), ty = fmaf(a.qdt2m, e[1], vn),
+                tz = fmaf(a.qdt2m, e[2], wn);
+    const float hx = e[3], hy = e[4], hz = e[5];
+    const float bsq = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+    const float inv = rcp_approx(fmaf(a.beta2, bsq, 1.0f));
+    const float tdb = fmaf(tx, hx, fmaf(ty, hy, tz * hz));
+    const float bt = a.beta * tdb;
+    const float cx = fmaf(ty, hz, -tz * hy), cy = fmaf(tz, hx, -tx * hz),
+                cz = fmaf(tx, hy, -ty * hx);
+    vbx = fmaf(a.beta, fmaf(bt, hx, cx), tx) * inv;
+    vby = fmaf(a.beta, fmaf(bt, hy, cy), ty) * inv;
+    vbz = fmaf(a.beta, fmaf(bt, hz, cz), tz) * inv;
+  }
+  float xo = fmaf(vbx, a.dt, xp), yo = fmaf(vby, a.dt, yp), zo = fmaf(vbz, a.dt, zp);
+  float uo = 2.0f * vbx - un, vo = 2.0f * vby - vn, wo = 2.0f * vbz - wn;
+  fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+  fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+  fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+  if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
+      zo > a.hi[2])
+    return ST_RUNAWAY;
+  xp = xo; yp = yo; zp = zo;
+  un = uo; vn = vo; wn = wo;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Deposition.  Lane L of a warp owns corner c = L & 7 of moments g, g + 4
+// (g = L >> 3) and, over half a tile, moment 8 + (g & 1).  Every tile's
+// staged particles are folded per cell in f32 (q * w_c * m) and added into a
+// per-warp node patch in shared memory: f32 sums over the nodes
+// [pi0, pi0 + PX) x [pj0, pj0 + 4) x [pk0, pk0 + 4) for the 10 moments — the
+// neighbourhood of the cells a chunk of sorted particles covers, strays
+// included.  Each lane only ever touches the patch values of its own
+// (corner, moment) pairs, so no atomics.  The patch is converted to the
+// lattice (x invvol x 2^43, rint) and flushed with REDG.ADD.64 when the chunk
+// ends or its cells leave the patch.
+template <int PX>
+struct Patch {
+  static constexpr int kNodes = PX * 16;       // node (px, py, pz) at (px * 4 + py) * 4 + pz
+  static constexpr int kStride = kNodes + 2;   // per moment; +2 spreads the lane groups over banks
+  static constexpr int kFloats = 10 * kStride;
+};
+
+// lattice value of a patch sum at global node `node`
+__device__ __forceinline__ long long lattice(const Params& a, float v, int node) {
+  const double iv = a.iv_d ? __ldg(a.iv_d + node) : (double)__ldg(a.iv_f + node);
+  return __double2ll_rn((double)v * iv * a.scale);
+}
+
+// Flush and clear the patch: each lane takes rows of 4 z-consecutive nodes.
+template <int PX>
+__device__ __forceinline__ void patch_flush(const Params& a, float* patch, int pi0, int pj0,
+                                            int pk0, unsigned lane) {
+  typedef Patch<PX> Pt;
+  for (int r = lane; r < 10 * PX * 4; r += 32) {
+    const int m = r / (PX * 4), rr = r - m * (PX * 4);
+    const int px = rr >> 2, py = rr & 3;
+    float* row = patch + m * Pt::kStride + rr * 4;
+    const float2 v01 = *reinterpret_cast<const float2*>(row);
+    const float2 v23 = *reinterpret_cast<const float2*>(row + 2);
+    if (v01.x != 0.f || v01.y != 0.f || v23.x != 0.f || v23.y != 0.f) {
+      const int node = ((pi0 + px) * a.NY + (pj0 + py)) * a.NZ + pk0;
+      long long* dst = a.acc + (size_t)m * a.NN + node;
+      const float vv[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+      for (int z = 0; z < 4; ++z)
+        if (vv[z] != 0.f)
+          atomicAdd(reinterpret_cast<unsigned long long*>(dst + z),
+                    (unsigned long long)lattice(a, vv[z], node + z));
+      *reinterpret_cast<float2*>(row) = make_float2(0.f, 0.f);
+      *reinterpret_cast<float2*>(row + 2) = make_float2(0.f, 0.f);
+    }
+  }
+}
+
+template <bool RX, bool RY, bool RZ, int PX, int CHUNK, int MINB>
+__global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ Params a) {
+  typedef Patch<PX> Pt;
+  extern __shared__ float smem_f[];
+  const unsigned lane = lane_id();
+  float* const st = smem_f + (threadIdx.x >> 5) * (kStage + Pt::kFloats);
+  float* const st_bs = st;             // [8][kRow] bases q * w_c
+  float* const st_mv = st + 8 * kRow;  // [10][kRow], row m = moment m (row 0: constant 1)
+  float* const patch = st + kStage;    // [10][kStride]
+  const int lc = lane & 7, lg = lane >> 3;
+  const int poff = (lc & 1) * 16 + ((lc >> 1) & 1) * 4 + ((lc >> 2) & 1);
+  const bool third = lg < 2;
+  const int m3 = 8 + (lg & 1), h3 = (lg >> 1) * 16;
+  // this lane's three patch value columns (moments lg, lg + 4, 8 + lg)
+  float* const pv0 = patch + lg * Pt::kStride + poff;
+  float* const pv1 = patch + (lg + 4) * Pt::kStride + poff;
+  float* const pv2 = patch + (third ? lg + 8 : 8) * Pt::kStride + poff;
+  st_mv[lane] = 1.0f;
+  for (int r = lane; r < Pt::kFloats; r += 32) patch[r] = 0.f;
+  __syncwarp();
+  int worst = ST_OK;
+  long long nxt = 0;
+  if (lane == 0) nxt = (long long)atomicAdd(a.work, (unsigned long long)CHUNK);
+  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  // prefetched particle of the next tile
+  float px_ = 0.f, py_ = 0.f, pz_ = 0.f, pu_ = 0.f, pv_ = 0.f, pw_ = 0.f, pq_ = 0.f;
+  auto fetch = [&](long long r, long long end) {
+    if (r < end) {
+      const long long p = a.start + r;
+      px_ = __ldcs(a.x + p); py_ = __ldcs(a.y + p); pz_ = __ldcs(a.z + p);
+      pu_ = __ldcs(a.u + p); pv_ = __ldcs(a.v + p); pw_ = __ldcs(a.w + p);
+      pq_ = __ldcs(a.q + p);
+    }
+  };
+  if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
+  while (nxt < a.count) {
+    const long long w0 = nxt;
+    const long long w1 = w0 + CHUNK < a.count ? w0 + CHUNK : a.count;
+    if (lane == 0) nxt = (long long)atomicAdd(a.work, (unsigned long long)CHUNK);
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+    int pi0 = 0, pj0 = 0, pk0 = 0;  // patch origin (node coordinates)
+    bool anchored = false;
+    for (long long t0 = w0; t0 < w1; t0 += 32) {
+      const long long r = t0 + lane;
+      bool valid = r < w1;
+      const long long p = a.start + r;
+      float xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_;
+      const float qp = pq_;
+      if (t0 + 32 < w1) fetch(t0 + 32 + lane, w1);
+      else if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
+      if (valid) {
+        const int s = push<RX, RY, RZ>(a, xp, yp, zp, un, vn, wn);
+        if (s != ST_OK) {
+          worst = s > worst ? s : worst;  // not stored, not deposited (kernels.py:618-621)
+          valid = false;
+        } else {
+          __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
+          __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
+        }
+      }
+      // ---- stage this lane's particle: 8 bases q*w_c and the moments
+      int ci = 0, cj = 0, ck = 0;
+      {
+        float fx = 0.f, fy = 0.f, fz = 0.f, qs = 0.f;
+        if (valid) {
+          cell_of(a, xp, yp, zp, fx, fy, fz, ci, cj, ck);
+          qs = qp;
+        }
+        const float qax = qs * (1.0f - fx), qfx = qs * fx;
+        const float ay = 1.0f - fy, az = 1.0f - fz;
+        const float w00 = qax * ay, w10 = qfx * ay, w01 = qax * fy, w11 = qfx * fy;
+        st_bs[0 * kRow + lane] = w00 * az; st_bs[1 * kRow + lane] = w10 * az;
+        st_bs[2 * kRow + lane] = w01 * az; st_bs[3 * kRow + lane] = w11 * az;
+        st_bs[4 * kRow + lane] = w00 * fz; st_bs[5 * kRow + lane] = w10 * fz;
+        st_bs[6 * kRow + lane] = w01 * fz; st_bs[7 * kRow + lane] = w11 * fz;
+        float* mv = st_mv + lane;
+        mv[1 * kRow] = un; mv[2 * kRow] = vn; mv[3 * kRow] = wn;
+        mv[4 * kRow] = un * un; mv[5 * kRow] = un * vn; mv[6 * kRow] = un * wn;
+        mv[7 * kRow] = vn * vn; mv[8 * kRow] = vn * wn; mv[9 * kRow] = wn * wn;
+      }
+      const unsigned V = __ballot_sync(0xffffffffu, valid);
+      if (V == 0u) continue;
+      // ---- patch placement
+      if (!anchored) {
+        anchored = true;
+        const int src = __ffs(V) - 1;
+        pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
+        pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
+        pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+      }
+      int dx = ci - pi0, dy = cj - pj0, dz = ck - pk0;
+      bool fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
+                 (unsigned)dz <= 2u;
+      unsigned F = __ballot_sync(0xffffffffu, fit);
+      if (__popc(V & ~F) > __popc(F)) {
+        // the run moved on: flush and re-anchor at its first particle outside
+        patch_flush<PX>(a, patch, pi0, pj0, pk0, lane);
+        const int src = __ffs(V & ~F) - 1;
+        pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
+        pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
+        pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+        dx = ci - pi0; dy = cj - pj0; dz = ck - pk0;
+        fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
+              (unsigned)dz <= 2u;
+        F = __ballot_sync(0xffffffffu, fit);
+      }
+      const int pnode = (dx * 4 + dy) * 4 + dz;  // patch node of corner 000 (fitting lanes)
+      // ---- main cell: the larger of the first / last fitting lane's cells
+      const int ka = __shfl_sync(0xffffffffu, pnode, __ffs(F | 1u) - 1);
+      const int kb = __shfl_sync(0xffffffffu, pnode, 31 - __clz(F | 1u));
+      const unsigned MA = __ballot_sync(0xffffffffu, fit && pnode == ka);
+      const unsigned MB = __ballot_sync(0xffffffffu, fit && pnode == kb);
+      const bool useb = __popc(MB) > __popc(MA);
+      const int kmain = useb ? kb : ka;
+      const unsigned Mm = useb ? MB : MA;
+      __syncwarp();
+      // ---- other cells of the tile: per-cell fold of their few particles
+      unsigned rest = F & ~Mm;
+      while (rest) {
+        const int src = __ffs(rest) - 1;
+        const int k2 = __shfl_sync(0xffffffffu, pnode, src);
+        const unsigned M2 = __ballot_sync(0xffffffffu, fit && pnode == k2);
+        rest &= ~M2;
+        float t0s = 0.f, t1s = 0.f, t2s = 0.f;
+        for (unsigned m = M2; m; m &= m - 1u) {
+          const int kk = __ffs(m) - 1;
+          const float b = st_bs[lc * kRow + kk];
+          t0s = fmaf(b, st_mv[lg * kRow + kk], t0s);
+          t1s = fmaf(b, st_mv[(lg + 4) * kRow + kk], t1s);
+          t2s = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], t2s);
+        }
+        pv0[k2] += t0s;
+        pv1[k2] += t1s;
+        if (third) pv2[k2] += t2s;
+      }
+      // ---- particles whose cells are outside the patch (rare): straight to the lattice
+      unsigned out = V & ~F;
+      while (out) {
+        const int src = __ffs(out) - 1;
+        const int oi = __shfl_sync(0xffffffffu, ci, src);
+        const int oj = __shfl_sync(0xffffffffu, cj, src);
+        const int ok = __shfl_sync(0xffffffffu, ck, src);
+        const unsigned M2 = __ballot_sync(0xffffffffu, valid && !fit && ci == oi && cj == oj &&
+                                                         ck == ok);
+        out &= ~M2;
+        float t0s = 0.f, t1s = 0.f, t2s = 0.f;
+        for (unsigned m = M2; m; m &= m - 1u) {
+          const int kk = __ffs(m) - 1;
+          const float b = st_bs[lc * kRow + kk];
+          t0s = fmaf(b, st_mv[lg * kRow + kk], t0s);
+          t1s = fmaf(b, st_mv[(lg + 4) * kRow + kk], t1s);
+          t2s = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], t2s);
+        }
+        const int node = ((oi + (lc & 1)) * a.NY + (oj + ((lc >> 1) & 1))) * a.NZ + ok +
+                         ((lc >> 2) & 1);
+        long long* dst = a.acc + (size_t)lg * a.NN + node;
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst),
+                  (unsigned long long)lattice(a, t0s, node));
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst + (size_t)4 * a.NN),
+                  (unsigned long long)lattice(a, t1s, node));
+        if (third)
+          atomicAdd(reinterpret_cast<unsigned long long*>(dst + (size_t)8 * a.NN),
+                    (unsigned long long)lattice(a, t2s, node));
+      }
+      if (V & ~Mm) {
+        if (((V & ~Mm) >> lane) & 1u) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) st_bs[c * kRow + lane] = 0.0f;
+        }
+        __syncwarp();
+      }
+      // ---- main fold: all 32 staged particles (others have zero bases)
+      if (Mm) {
+        const float* br = st_bs + lc * kRow;
+        const float* m0r = st_mv + lg * kRow;
+        const float* m1r = st_mv + (lg + 4) * kRow;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 4) {
+          const float4 b = *reinterpret_cast<const float4*>(br + kk);
+          const float4 x0 = *reinterpret_cast<const float4*>(m0r + kk);
+          const float4 x1 = *reinterpret_cast<const float4*>(m1r + kk);
+          s0 = fmaf(b.x, x0.x, s0); s0 = fmaf(b.y, x0.y, s0);
+          s0 = fmaf(b.z, x0.z, s0); s0 = fmaf(b.w, x0.w, s0);
+          s1 = fmaf(b.x, x1.x, s1); s1 = fmaf(b.y, x1.y, s1);
+          s1 = fmaf(b.z, x1.z, s1); s1 = fmaf(b.w, x1.w, s1);
+        }
+        const float* b3 = st_bs + lc * kRow + h3;
+        const float* m3r = st_mv + m3 * kRow + h3;
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4) {
+          const float4 b = *reinterpret_cast<const float4*>(b3 + kk);
+          const float4 x2 = *reinterpret_cast<const float4*>(m3r + kk);
+          s2 = fmaf(b.x, x2.x, s2); s2 = fmaf(b.y, x2.y, s2);
+          s2 = fmaf(b.z, x2.z, s2); s2 = fmaf(b.w, x2.w, s2);
+        }
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 16);
+        pv0[kmain] += s0;
+        pv1[kmain] += s1;
+        if (third) pv2[kmain] += s2;
+      }
+      __syncwarp();
+    }
+    if (anchored) patch_flush<PX>(a, patch, pi0, pj0, pk0, lane);
+    __syncwarp();
+  }
+  if (worst != ST_OK) atomicMax(a.status, worst);
+}
+
+// Per-cell coefficient records (computed in f64, rounded once to f32):
+// float4 2m = (c0, c1, c2, c4), 2m+1 = (c3, c5, c6, c7) of component m
+// (Ex Ey Ez Bx By Bz).
+template <typename F>
+__global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int nx, int ny,
+                           int nz, float4* __restrict__ rec) {
+  const int NY = ny + 1, NZ = nz + 1, NN = (nx + 1) * NY * NZ;
+  const int ncell = nx * ny * nz;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+    const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+    const int n0 = (i * NY + j) * NZ + k;
+    const int sx = NY * NZ, sy = NZ;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      const F* f = (m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN) + n0;
+      const double f000 = f[0], f100 = f[sx], f010 = f[sy], f110 = f[sx + sy];
+      const double f001 = f[1], f101 = f[sx + 1], f011 = f[sy + 1], f111 = f[sx + sy + 1];
+      const double c1 = f100 - f000, c2 = f010 - f000, c3 = f001 - f000;
+      const double c4 = (f110 - f100) - (f010 - f000);
+      const double c5 = (f101 - f001) - (f100 - f000);
+      const double c6 = (f011 - f001) - (f010 - f000);
+      const double c7 = ((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000));
+      rec[(size_t)c * 12 + 2 * m] = make_float4((float)f000, (float)c1, (float)c2, (float)c4);
+      rec[(size_t)c * 12 + 2 * m + 1] = make_float4((float)c3, (float)c5, (float)c6, (float)c7);
+    }
+  }
+}
+
+}  // namespace f32k
+
+namespace {
+
+// kernel shape: patch width, chunk, blocks per SM (BP_F32_CFG=0/1 picks one)
+template <bool RX, bool RY, bool RZ, int PX, int CHUNK, int MINB>
+int launch_cfg(const f32k::Params& a, cudaStream_t s) {
+  auto k = f32k::fused_f32<RX, RY, RZ, PX, CHUNK, MINB>;
+  const size_t smem =
+      (size_t)(256 / 32) * (f32k::kStage + f32k::Patch<PX>::kFloats) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long need = (a.count + 255) / 256;
+  long long g = (long long)sms * per_sm;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(int)g, 256, smem, s>>>(a);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("f32 fused kernel launch: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+template <bool RX, bool RY, bool RZ>
+int launch_bc(const f32k::Params& a, cudaStream_t s) {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* env = getenv("BP_F32_CFG");
+    cfg = env ? atoi(env) : 0;
+  }
+  if (cfg == 1) return launch_cfg<RX, RY, RZ, 12, 1024, 2>(a, s);
+  return launch_cfg<RX, RY, RZ, 8, 512, 3>(a, s);
+}
+
+}  // namespace
+
+// Number of bytes of cell records for a grid (12 float4 per cell).
+size_t f32_records_bytes(const int64_t* geo_i) {
+  return (size_t)geo_i[0] * geo_i[1] * geo_i[2] * 12 * sizeof(float4);
+}
+
+int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* geo_i,
+                     void* rec, cudaStream_t s) {
+  const int nx = (int)geo_i[0], ny = (int)geo_i[1], nz = (int)geo_i[2];
+  const long long ncell = (long long)nx * ny * nz;
+  int blocks = (int)((ncell + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (fbytes == 8)
+    f32k::pack_cells<double><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B, nx, ny,
+                                                     nz, (float4*)rec);
+  else
+    f32k::pack_cells<float><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B, nx, ny, nz,
+                                                    (float4*)rec);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("cell record pack: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+// Fused f32 launch with prebuilt records (rec) or, when rec == NULL, records
+// built on the stream for this call.
+int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
+  f32k::Params a;
+  a.x = (float*)c.x; a.y = (float*)c.y; a.z = (float*)c.z;
+  a.u = (float*)c.u; a.v = (float*)c.v; a.w = (float*)c.w;
+  a.q = (const float*)c.q;
+  a.start = c.start; a.count = c.count;
+  a.iv_f = c.fbytes == 4 ? (const float*)c.invvol : nullptr;
+  a.iv_d = c.fbytes == 8 ? (const double*)c.invvol : nullptr;
+  a.acc = (long long*)c.acc;
+  a.nx = (int)c.geo_i[0]; a.ny = (int)c.geo_i[1]; a.nz = (int)c.geo_i[2];
+  a.NY = a.ny + 1; a.NZ = a.nz + 1; a.NN = (a.nx + 1) * a.NY * a.NZ;
+  a.cny = a.nx * a.ny;
+  for (int k = 0; k < 3; ++k) {
+    const float o = (float)c.geo_f[3 + k], L = (float)c.geo_f[6 + k];
+    const float hi = o + L;  // f32 sum, as the reference's single/mixed modes
+    a.o[k] = o; a.L[k] = L; a.hi[k] = hi; a.hi2[k] = hi + hi;
+    const double gd = (double)(c.fbytes == 8 ? c.geo_g[k] : (double)(float)c.geo_g[k]);
+    const double go = (double)(c.fbytes == 8 ? c.geo_g[3 + k] : (double)(float)c.geo_g[3 + k]);
+    a.idx[k] = (float)(1.0 / gd);
+    a.ogs[k] = (float)(go / gd);
+  }
+  a.dt = (float)c.dt; a.dth = (float)c.dth; a.qdt2m = (float)c.qdt2m;
+  a.beta = (float)c.beta;
+  a.beta2 = a.beta * a.beta;
+  a.scale = c.scale;
+  a.n_iters = c.n_iters;
+  a.status = c.status;
+  void* rec = const_cast<void*>(rec_in);
+  const size_t rbytes = f32_records_bytes(c.geo_i);
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, (rec ? 0 : rbytes) + 256, s);
+  if (e != cudaSuccess) {
+    set_error("f32 scratch alloc: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  a.work = (unsigned long long*)scratch;
+  cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), s);
+  int rc = 0;
+  if (!rec) {
+    rec = (char*)scratch + 256;
+    rc = f32_pack_records(c.fbytes, c.E, c.B, c.geo_i, rec, s);
+  }
+  a.rec = (const float4*)rec;
+  if (!rc) {
+    const int m = (c.geo_i[3] ? 1 : 0) | (c.geo_i[4] ? 2 : 0) | (c.geo_i[5] ? 4 : 0);
+    switch (m) {
+      case 0: rc = launch_bc<false, false, false>(a, s); break;
+      case 1: rc = launch_bc<true, false, false>(a, s); break;
+      case 2: rc = launch_bc<false, true, false>(a, s); break;
+      case 3: rc = launch_bc<true, true, false>(a, s); break;
+      case 4: rc = launch_bc<false, false, true>(a, s); break;
+      case 5: rc = launch_bc<true, false, true>(a, s); break;
+      case 6: rc = launch_bc<false, true, true>(a, s); break;
+      default: rc = launch_bc<true, true, true>(a, s); break;
+    }
+  }
+  cudaFreeAsync(scratch, s);
+  return rc;
+}
+
+}  // namespace bp

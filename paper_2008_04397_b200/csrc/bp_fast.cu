@@ -22,6 +22,12 @@ int dispatch(const Call& c, cudaStream_t s) {
 }  // namespace
 
 int launch_fast(const Call& c, cudaStream_t s) {
+  // f32 particles, fused: the dedicated kernel of bp_f32.cu (BP_F32_GENERIC=1
+  // selects the generic policy kernel instead, for comparisons)
+  if (c.op == OP_FUSED && c.pbytes == 4) {
+    const char* env = getenv("BP_F32_GENERIC");
+    if (!(env && env[0] == '1')) return f32_fused(c, nullptr, s);
+  }
   if (c.pbytes == 8 && c.fbytes == 8) return dispatch<double, double>(c, s);
   if (c.pbytes == 4 && c.fbytes == 4) return dispatch<float, float>(c, s);
   if (c.pbytes == 4 && c.fbytes == 8) return dispatch<float, double>(c, s);

@@ -33,6 +33,14 @@ int launch_fast(const Call& c, cudaStream_t s);
 
 void set_error(const char* fmt, ...);
 
+// f32 particles, fast arithmetic, fused op (bp_f32.cu): per-cell coefficient
+// records `rec` (f32_records_bytes) prebuilt by f32_pack_records, or NULL to
+// build them on the stream for this call.
+size_t f32_records_bytes(const int64_t* geo_i);
+int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* geo_i, void* rec,
+                     cudaStream_t s);
+int f32_fused(const Call& c, const void* rec, cudaStream_t s);
+
 // count of kernels this library launched (bp_kernel_launches)
 void note_launch(int n = 1);
 

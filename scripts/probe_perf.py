@@ -21,19 +21,21 @@ pd, fd = {"double": (torch.float64, torch.float64), "single": (torch.float32, to
           "mixed": (torch.float32, torch.float64)}[mode]
 npd = np.float64 if pd == torch.float64 else np.float32
 nfd = np.float64 if fd == torch.float64 else np.float32
-geom = GridGeometry.from_box((128, 64, 64), (25.6, 12.8, 12.8), bc=("periodic", "reflecting", "periodic"))
+cells = tuple(int(c) for c in os.environ.get("PROBE_CELLS", "128,64,64").split(","))
+geom = GridGeometry.from_box(cells, tuple(0.2 * c for c in cells), bc=("periodic", "reflecting", "periodic"))
+vth = float(os.environ.get("PROBE_VTH", "0.0224"))
 dev = torch.device("cuda")
 nc = geom.n_cells
 n = nc * ppc
 g = torch.Generator(device=dev); g.manual_seed(1)
 cell = torch.arange(nc, device=dev).repeat_interleave(ppc)
-ci = cell % 128; cj = (cell // 128) % 64; ck = cell // (128 * 64)
+ci = cell % cells[0]; cj = (cell // cells[0]) % cells[1]; ck = cell // (cells[0] * cells[1])
 x = ((ci + torch.rand(n, device=dev, generator=g, dtype=torch.float64)) * geom.dx).to(pd)
 y = ((cj + torch.rand(n, device=dev, generator=g, dtype=torch.float64)) * geom.dy).to(pd)
 z = ((ck + torch.rand(n, device=dev, generator=g, dtype=torch.float64)) * geom.dz).to(pd)
-u = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * 0.0224).to(pd)
-v = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * 0.0224).to(pd)
-w = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * 0.0224).to(pd)
+u = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * vth).to(pd)
+v = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * vth).to(pd)
+w = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * vth).to(pd)
 q = torch.full((n,), -1e-4, device=dev, dtype=pd)
 shp = (3,) + geom.node_shape
 E = (torch.randn(shp, device=dev, generator=g, dtype=torch.float64) * 1e-3).to(fd)

@@ -264,3 +264,28 @@ def test_tma_stream_path_matches(gpu, oracle, tma_stream, monkeypatch, mode, ari
             oracle.fused_span(*ref, start, count, E, B, acc_ref, inv, *tail)
             assert np.array_equal(acc_ref, dacc.cpu().numpy())
             assert all(np.array_equal(r, t.cpu().numpy()) for r, t in zip(ref, d))
+
+
+@pytest.mark.parametrize("mode", ["single", "mixed"])
+def test_fast_f32_fused_is_deterministic(gpu, mode):
+    """The f32 fused kernel (bp_f32.cu) claims work dynamically but flushes
+    every chunk's sums on its own, so repeated launches give identical bits."""
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 250_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(mode, n, seed=41,
+                                                                       order="sorted")
+    inv = geom.inv_node_volume(fd)
+    mixed = 1 if pd != fd else 0
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+            fd(SCALE), mixed)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    outs = []
+    for _ in range(3):
+        d = _dev(torch, arrs)
+        dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+        K.fused_span(*d, 0, n, dE, dB, dacc, dinv, *tail, arith="fast")
+        outs.append((dacc, d))
+    for dacc, d in outs[1:]:
+        assert torch.equal(dacc, outs[0][0])
+        assert all(torch.equal(a, b) for a, b in zip(d, outs[0][1]))

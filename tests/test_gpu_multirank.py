@@ -1,7 +1,11 @@
 """Particle decomposition on the device path: two ranks (gloo, sharing one
 GPU) each push their shard of every species and all-reduce the int64
 moments; the result must be bit-identical to one rank pushing everything
-(the exact lattice makes the moment merge order-free)."""
+(the exact lattice makes the moment merge order-free).
+
+Fast f32 arithmetic rounds per-tile f32 partial sums onto the lattice
+(bp_f32.cu), so its moments depend on how particles fall into tiles: the
+particles stay bitwise, the moments agree within the f32 tolerance."""
 
 import os
 import socket
@@ -20,7 +24,7 @@ def _port():
     return p
 
 
-def _run(rank, world, port, arith, out):
+def _run(rank, world, port, arith, label, out):
     import torch
     import torch.distributed as dist
     from paper_2008_04397_b200.config import PrecisionMode
@@ -33,7 +37,7 @@ def _run(rank, world, port, arith, out):
     torch.cuda.set_device(0)
     geom = gem_geometry((16, 8, 8), (6.4, 3.2, 3.2))
     species = gem_species(8)
-    prec = PrecisionMode.from_label("single")
+    prec = PrecisionMode.from_label(label)
     bufs, fields = init_gem_host(geom, species, GemInit(seed=3), prec)
     sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=arith, sort_period=2,
                            distributed=distributed)
@@ -49,17 +53,25 @@ def _run(rank, world, port, arith, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("arith", ["parity", "fast"])
-def test_two_ranks_bitwise_equal_one_rank(gpu, arith):
+@pytest.mark.parametrize("arith,label", [("parity", "single"), ("fast", "double"),
+                                         ("fast", "single")])
+def test_two_ranks_bitwise_equal_one_rank(gpu, arith, label):
     import torch.multiprocessing as mp
+    exact = not (arith == "fast" and label != "double")
     with mp.Manager() as m:
         one = m.dict()
-        mp.spawn(_run, args=(1, 0, arith, one), nprocs=1, join=True)
+        mp.spawn(_run, args=(1, 0, arith, label, one), nprocs=1, join=True)
         two = m.dict()
-        mp.spawn(_run, args=(2, _port(), arith, two), nprocs=2, join=True)
+        mp.spawn(_run, args=(2, _port(), arith, label, two), nprocs=2, join=True)
         a1, a2 = one["accs"], two["accs"]
         for x, y in zip(a1, a2):
-            assert np.array_equal(x, y)
+            if exact:
+                assert np.array_equal(x, y)
+            else:
+                for r in range(x.shape[0]):
+                    ref = x[r].astype(np.float64)
+                    err = np.abs(y[r] - ref).max() / max(np.abs(ref).max(), 1.0)
+                    assert err <= 1e-5, (r, err)
         for s in range(4):
             ids1, x1, u1 = one["parts0"][s]
             ids = np.concatenate([two["parts0"][s][0], two["parts1"][s][0]])

@@ -91,7 +91,9 @@ def test_c1_replay_fast_within_tolerance(gpu, mode):
 def test_sorting_toggle_changes_nothing_bitwise(gpu, arith):
     """The reference's C9 / test_pipeline.py:146-152 on the device path: with
     and without the periodic on-device sort, particles (matched by id) and
-    moments are bit-identical after 10 cycles."""
+    moments are bit-identical after 10 cycles (fast f32 arithmetic: the
+    particles bitwise, the moments — per-tile f32 partial sums, bp_f32.cu —
+    within the f32 tolerance)."""
     from paper_2008_04397_b200.config import PrecisionMode
     from paper_2008_04397_b200.gem import GemInit, gem_geometry, gem_species, init_gem_host
     from paper_2008_04397_b200.pipeline import DeviceSimulation
@@ -109,7 +111,13 @@ def test_sorting_toggle_changes_nothing_bitwise(gpu, arith):
         out.append(([p.to_host() for p in sim.particles], sim.moments_host()))
     (pa, ma), (pb, mb) = out
     for x, y in zip(ma, mb):
-        assert np.array_equal(x, y)
+        if arith == "parity":
+            assert np.array_equal(x, y)
+        else:
+            for r in range(x.shape[0]):
+                ref = x[r].astype(np.float64)
+                err = np.abs(y[r] - ref).max() / max(np.abs(ref).max(), 1.0)
+                assert err <= 1e-5, (r, err)
     for a, b in zip(pa, pb):
         oa, ob = np.argsort(a.ids), np.argsort(b.ids)
         for nm in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
