@@ -114,6 +114,26 @@ int bp_fused_span_ex(int arith, int pbytes, int fbytes, void* xs, void* ys, void
                      double dth, double qdt2m, double beta, double one, int n_iters,
                      double scale, int mixed, int* d_status, void* stream);
 
+/* Per-cell field records for the f32 fast kernels (bp_f32.cu): for every
+ * cell the trilinear coefficients of Ex Ey Ez Bx By Bz (48 floats).  The
+ * fused call builds them from E / B on its stream unless the caller passes
+ * records built once per field update: bp_field_records_bytes() gives the
+ * size of the (32-byte aligned) device buffer, bp_field_records_build()
+ * fills it from E, B (fbytes 4 or 8), and bp_fused_span_rec() is
+ * bp_fused_span_ex() with a `records` argument (NULL = build per call;
+ * ignored by the parity and f64 kernels).  The records must describe the E,
+ * B passed to the call. */
+int64_t bp_field_records_bytes(const int64_t* geo_i);
+int bp_field_records_build(int fbytes, const void* E, const void* B, const int64_t* geo_i,
+                           void* records, void* stream);
+int bp_fused_span_rec(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
+                      void* vs, void* ws, const void* qs, int64_t start, int64_t count,
+                      const void* E, const void* B, int64_t* acc, const void* invvol,
+                      const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
+                      double dth, double qdt2m, double beta, double one, int n_iters,
+                      double scale, int mixed, const void* records, int* d_status,
+                      void* stream);
+
 /* Host-memory variant of bp_fused_span: particle arrays, E, B, acc and invvol
  * are HOST pointers (pinned or pageable).  The span is streamed through the
  * device in batches of at most batch_particles (0 = automatic) with

@@ -28,6 +28,7 @@ EXPORTS = (
     "bp_deposit_span", "bp_gather_span", "bp_fused_span_ex",
     "bp_fused_span_host", "bp_sort_by_cell", "bp_sort_by_cell_into", "bp_cell_keys",
     "bp_fold_periodic_i64", "bp_moments_total", "bp_susceptibility",
+    "bp_field_records_bytes", "bp_field_records_build", "bp_fused_span_rec",
 )
 
 _P = ctypes.c_void_p
@@ -44,6 +45,11 @@ _SIGS = {
     "bp_fused_span_ex": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]
                          + [_P] * 4 + [_P, _P, _P] + [_D] * 5
                          + [_INT, _D, _INT, _P, _P]),
+    "bp_fused_span_rec": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]
+                          + [_P] * 4 + [_P, _P, _P] + [_D] * 5
+                          + [_INT, _D, _INT, _P, _P, _P]),
+    "bp_field_records_bytes": (_I64, [_P]),
+    "bp_field_records_build": (_INT, [_INT, _P, _P, _P, _P, _P]),
     "bp_push_span": (_INT, [_INT, _INT] + [_P] * 6 + [_I64, _I64, _P, _P]
                      + [_P, _P, _P] + [_D] * 5 + [_INT, _INT, _INT, _P, _P]),
     "bp_deposit_span": (_INT, [_INT, _INT] + [_P] * 7 + [_I64, _I64, _P, _P,

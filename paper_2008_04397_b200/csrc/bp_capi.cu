@@ -166,7 +166,7 @@ int fused_call(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, 
                const void* B, int64_t* acc, const void* invvol, const double* geo_f,
                const double* geo_g, const int64_t* geo_i, double dt, double dth, double qdt2m,
                double beta, double one, int n_iters, double scale, int mixed, int* d_status,
-               cudaStream_t s) {
+               cudaStream_t s, const void* records = nullptr) {
   if (!valid_pair(pbytes, fbytes)) {
     set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
     return BP_EINVAL;
@@ -186,6 +186,7 @@ int fused_call(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, 
   fill_geo(c, geo_f, geo_g, geo_i);
   c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
   c.n_iters = n_iters; c.mixed = mixed; c.apply_bc = 1;
+  c.records = records;
   return run(c, arith, d_status, s);
 }
 
@@ -281,6 +282,51 @@ int bp_fused_span_ex(int arith, int pbytes, int fbytes, void* xs, void* ys, void
   return fused_call(arith, pbytes, fbytes, xs, ys, zs, us, vs, ws, qs, start, count, E, B, acc,
                     invvol, geo_f, geo_g, geo_i, dt, dth, qdt2m, beta, one, n_iters, scale,
                     mixed, d_status, (cudaStream_t)stream);
+}
+
+int64_t bp_field_records_bytes(const int64_t* geo_i) {
+  if (!geo_i || geo_i[0] < 1 || geo_i[1] < 1 || geo_i[2] < 1) {
+    set_error("cell counts must be >= 1");
+    return BP_EINVAL;
+  }
+  return (int64_t)f32_records_bytes(geo_i);
+}
+
+int bp_field_records_build(int fbytes, const void* E, const void* B, const int64_t* geo_i,
+                           void* records, void* stream) {
+  if (fbytes != 4 && fbytes != 8) {
+    set_error("field dtype must be 4 or 8 bytes");
+    return BP_EINVAL;
+  }
+  if (!E || !B || !records || !geo_i) {
+    set_error("E, B, geo_i and records are required");
+    return BP_EINVAL;
+  }
+  if (geo_i[0] < 1 || geo_i[1] < 1 || geo_i[2] < 1) {
+    set_error("cell counts must be >= 1");
+    return BP_EINVAL;
+  }
+  if (((uintptr_t)records % 32) != 0) {
+    set_error("records must be 32-byte aligned");
+    return BP_EINVAL;
+  }
+  return f32_pack_records(fbytes, E, B, geo_i, records, (cudaStream_t)stream) ? BP_ECUDA : BP_OK;
+}
+
+int bp_fused_span_rec(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
+                      void* vs, void* ws, const void* qs, int64_t start, int64_t count,
+                      const void* E, const void* B, int64_t* acc, const void* invvol,
+                      const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
+                      double dth, double qdt2m, double beta, double one, int n_iters,
+                      double scale, int mixed, const void* records, int* d_status,
+                      void* stream) {
+  if (records && ((uintptr_t)records % 32) != 0) {
+    set_error("records must be 32-byte aligned");
+    return BP_EINVAL;
+  }
+  return fused_call(arith, pbytes, fbytes, xs, ys, zs, us, vs, ws, qs, start, count, E, B, acc,
+                    invvol, geo_f, geo_g, geo_i, dt, dth, qdt2m, beta, one, n_iters, scale,
+                    mixed, d_status, (cudaStream_t)stream, records);
 }
 
 int bp_push_span(int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us, void* vs,

@@ -6,9 +6,13 @@
 // Push: fields come from per-cell coefficient records (pack_cells): for each
 // component f the trilinear form
 //     f(fx,fy,fz) = [c0 + c1 fx + (c2 + c4 fx) fy] + fz [c3 + c5 fx + (c6 + c7 fx) fy]
-// (the reference's 8-weight sum, kernels.py:557-591, regrouped), so one gather
-// is 12 contiguous 16-byte loads from one 192-byte record and 7 FFMA per
-// component.  Boundary kinds are template parameters.
+// (the reference's 8-weight sum, kernels.py:557-591, regrouped).  Components
+// are paired (Ex Ey | Bx By | Ez Bz) and evaluated with the packed FP32
+// instruction FFMA2 (two lanes of f32 per instruction, sm_100), so one gather
+// is 12 contiguous 16-byte loads from one 192-byte record and 21 FFMA2; the
+// record stays in registers while the midpoint remains in its cell, so the
+// mover iterations after the first usually load nothing.  Boundary kinds are
+// template parameters.
 //
 // Deposit: the per-warp transposed fold of bp_common.cuh (lane = corner x
 // moment group, 32 staged particles per tile) in f32: each tile's partial sum
@@ -43,7 +47,8 @@ struct Params {
   double scale;
   int n_iters;
   int* status;
-  unsigned long long* work;
+  unsigned long long* work;  // deposit: next unclaimed particle of the span
+  unsigned* skip;            // one bit per span particle the mover did not store
 };
 
 constexpr int kRow = 36;  // staged row stride (floats): conflict-free LDS.128 per warp
@@ -63,6 +68,13 @@ __device__ __forceinline__ float rcp_approx(float d) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
   return r;
+}
+
+// one 32-byte load (LDG.E.ENL2.256) into two float4
+__device__ __forceinline__ void ldg8(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
 }
 
 template <bool REFL>
@@ -114,21 +126,32 @@ __device__ __forceinline__ int cell_of(const Params& a, float x, float y, float 
   return i + a.nx * j + a.cny * k;
 }
 
-// one component from its two coefficient quads
-__device__ __forceinline__ float tri(const float4 A, const float4 B, float fx, float fy,
-                                     float fz) {
-  const float p = fmaf(A.y, fx, A.x), q = fmaf(A.w, fx, A.z);
-  const float r = fmaf(B.y, fx, B.x), s = fmaf(B.w, fx, B.z);
-  return fmaf(fmaf(s, fy, r), fz, fmaf(q, fy, p));
+typedef float2 F2;
+__device__ __forceinline__ F2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) { return __fmul2_rn(a, b); }
+
+// one component pair from its four coefficient quads (record layout of
+// pack_cells: A = c0 c0' c1 c1', B = c2 c2' c4 c4', C = c3 c3' c5 c5', D = c6 c6' c7 c7')
+__device__ __forceinline__ F2 tri2(const float4& A, const float4& B, const float4& C,
+                                   const float4& D, F2 FX, F2 FY, F2 FZ) {
+  const F2 p = fma2(f2(A.z, A.w), FX, f2(A.x, A.y));
+  const F2 q = fma2(f2(B.z, B.w), FX, f2(B.x, B.y));
+  const F2 r = fma2(f2(C.z, C.w), FX, f2(C.x, C.y));
+  const F2 t = fma2(f2(D.z, D.w), FX, f2(D.x, D.y));
+  return fma2(fma2(t, FY, r), FZ, fma2(q, FY, p));
 }
 
-template <bool RX, bool RY, bool RZ>
+template <bool RX, bool RY, bool RZ, bool REUSE>
 __device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float& zp, float& un,
                                     float& vn, float& wn) {
   float vbx = un, vby = vn, vbz = wn;
+  float4 R[12];
+  int held = -1;  // cell whose record is in R
 #pragma unroll 1
   for (int it = 0; it < a.n_iters; ++it) {
-    float xm = fmaf(vbx, a.dth, xp), ym = fmaf(vby, a.dth, yp), zm = fmaf(vbz, a.dth, zp);
+    const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
+    float xm = XM.x, ym = XM.y, zm = fmaf(vbz, a.dth, zp);
     xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
     ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
     zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
@@ -138,13 +161,19 @@ __device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float
     float fx, fy, fz;
     int i, j, k;
     const int cell = cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
-    const float4* r = a.rec + (size_t)cell * 12;
-    float e[6];
+    if (!REUSE || cell != held) {
+      held = cell;
+      const float4* r = a.rec + (size_t)cell * 12;
 #pragma unroll
-    for (int m = 0; m < 6; ++m) e[m] = tri(ldg4(r + 2 * m), ldg4(r + 2 * m + 1), fx, fy, fz);
-    const float tx = fmaf(a.qdt2m, e[0], un), ty = fmaf(a.qdt2m, e[1], vn),
-                tz = fmaf(a.qdt2m, e[2], wn);
-    const float hx = e[3], hy = e[4], hz = e[5];
+      for (int q = 0; q < 12; q += 2) ldg8(r + q, R[q], R[q + 1]);
+    }
+    const F2 FX = f2(fx, fx), FY = f2(fy, fy), FZ = f2(fz, fz);
+    const F2 Exy = tri2(R[0], R[1], R[2], R[3], FX, FY, FZ);
+    const F2 Bxy = tri2(R[4], R[5], R[6], R[7], FX, FY, FZ);
+    const F2 EBz = tri2(R[8], R[9], R[10], R[11], FX, FY, FZ);
+    const F2 Txy = fma2(f2(a.qdt2m, a.qdt2m), Exy, f2(un, vn));
+    const float tx = Txy.x, ty = Txy.y, tz = fmaf(a.qdt2m, EBz.x, wn);
+    const float hx = Bxy.x, hy = Bxy.y, hz = EBz.y;
     const float bsq = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
     const float inv = rcp_approx(fmaf(a.beta2, bsq, 1.0f));
     const float tdb = fmaf(tx, hx, fmaf(ty, hy, tz * hz));
@@ -218,8 +247,53 @@ __device__ __forceinline__ void patch_flush(const Params& a, float* patch, int p
   }
 }
 
-template <bool RX, bool RY, bool RZ, int PX, int CHUNK, int MINB>
-__global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ Params a) {
+// ---------------------------------------------------------------------------
+// Mover: one particle per thread, coalesced SoA streams, no shared memory, so
+// the SM holds enough warps to hide the latency of the three dependent
+// gather + rotation steps.  Particles that fail (kernels.py:618-621, 672-676)
+// are not stored; their bit in `skip` keeps them out of the deposit.
+template <bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+__global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ Params a) {
+  // persistent grid: each thread walks particles r, r + stride, ... with the
+  // next particle's loads in flight while the current one is pushed
+  const long long stride = (long long)gridDim.x * 256;
+  long long r = (long long)blockIdx.x * 256 + threadIdx.x;
+  float nx_ = 0.f, ny_ = 0.f, nz_ = 0.f, nu_ = 0.f, nv_ = 0.f, nw_ = 0.f;
+  auto fetch = [&](long long rr) {
+    if (rr < a.count) {
+      const long long p = a.start + rr;
+      nx_ = __ldcs(a.x + p); ny_ = __ldcs(a.y + p); nz_ = __ldcs(a.z + p);
+      nu_ = __ldcs(a.u + p); nv_ = __ldcs(a.v + p); nw_ = __ldcs(a.w + p);
+    }
+  };
+  fetch(r);
+  const long long rbase = r - (threadIdx.x & 31);  // warp-uniform loop bound
+  for (long long rb = rbase; rb < a.count; rb += stride, r += stride) {
+    float xp = nx_, yp = ny_, zp = nz_, un = nu_, vn = nv_, wn = nw_;
+    fetch(r + stride);
+    int st = ST_OK;
+    if (r < a.count) {
+      const long long p = a.start + r;
+      st = push<RX, RY, RZ, REUSE>(a, xp, yp, zp, un, vn, wn);
+      if (st == ST_OK) {
+        __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
+        __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
+      }
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, st != ST_OK);
+    if (bad) {
+      if ((threadIdx.x & 31) == 0) atomicOr(a.skip + (r >> 5), bad);
+      if (st != ST_OK) atomicMax(a.status, st);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deposit (interpolation of the 10 moments) of the moved particles.  Each
+// warp claims chunks of CHUNK particles; tiles of 32 are staged in shared
+// memory and folded per cell (see the comment above Patch).
+template <int PX, int CHUNK, int MINB>
+__global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__ Params a) {
   typedef Patch<PX> Pt;
   extern __shared__ float smem_f[];
   const unsigned lane = lane_id();
@@ -238,12 +312,12 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
   st_mv[lane] = 1.0f;
   for (int r = lane; r < Pt::kFloats; r += 32) patch[r] = 0.f;
   __syncwarp();
-  int worst = ST_OK;
   long long nxt = 0;
   if (lane == 0) nxt = (long long)atomicAdd(a.work, (unsigned long long)CHUNK);
   nxt = __shfl_sync(0xffffffffu, nxt, 0);
   // prefetched particle of the next tile
   float px_ = 0.f, py_ = 0.f, pz_ = 0.f, pu_ = 0.f, pv_ = 0.f, pw_ = 0.f, pq_ = 0.f;
+  unsigned sk_ = 0u;
   auto fetch = [&](long long r, long long end) {
     if (r < end) {
       const long long p = a.start + r;
@@ -251,6 +325,7 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
       pu_ = __ldcs(a.u + p); pv_ = __ldcs(a.v + p); pw_ = __ldcs(a.w + p);
       pq_ = __ldcs(a.q + p);
     }
+    sk_ = __ldg(a.skip + (r >> 5));
   };
   if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
   while (nxt < a.count) {
@@ -262,22 +337,10 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
     bool anchored = false;
     for (long long t0 = w0; t0 < w1; t0 += 32) {
       const long long r = t0 + lane;
-      bool valid = r < w1;
-      const long long p = a.start + r;
-      float xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_;
-      const float qp = pq_;
+      const bool valid = r < w1 && !((sk_ >> lane) & 1u);
+      const float xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_, qp = pq_;
       if (t0 + 32 < w1) fetch(t0 + 32 + lane, w1);
       else if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
-      if (valid) {
-        const int s = push<RX, RY, RZ>(a, xp, yp, zp, un, vn, wn);
-        if (s != ST_OK) {
-          worst = s > worst ? s : worst;  // not stored, not deposited (kernels.py:618-621)
-          valid = false;
-        } else {
-          __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
-          __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
-        }
-      }
       // ---- stage this lane's particle: 8 bases q*w_c and the moments
       int ci = 0, cj = 0, ck = 0;
       {
@@ -337,8 +400,7 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
       // ---- other cells of the tile: per-cell fold of their few particles
       unsigned rest = F & ~Mm;
       while (rest) {
-        const int src = __ffs(rest) - 1;
-        const int k2 = __shfl_sync(0xffffffffu, pnode, src);
+        const int k2 = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
         const unsigned M2 = __ballot_sync(0xffffffffu, fit && pnode == k2);
         rest &= ~M2;
         float t0s = 0.f, t1s = 0.f, t2s = 0.f;
@@ -394,16 +456,16 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
         const float* br = st_bs + lc * kRow;
         const float* m0r = st_mv + lg * kRow;
         const float* m1r = st_mv + (lg + 4) * kRow;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        F2 S0 = f2(0.f, 0.f), S1 = f2(0.f, 0.f), S2 = f2(0.f, 0.f);
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 4) {
           const float4 b = *reinterpret_cast<const float4*>(br + kk);
           const float4 x0 = *reinterpret_cast<const float4*>(m0r + kk);
           const float4 x1 = *reinterpret_cast<const float4*>(m1r + kk);
-          s0 = fmaf(b.x, x0.x, s0); s0 = fmaf(b.y, x0.y, s0);
-          s0 = fmaf(b.z, x0.z, s0); s0 = fmaf(b.w, x0.w, s0);
-          s1 = fmaf(b.x, x1.x, s1); s1 = fmaf(b.y, x1.y, s1);
-          s1 = fmaf(b.z, x1.z, s1); s1 = fmaf(b.w, x1.w, s1);
+          S0 = fma2(f2(b.x, b.y), f2(x0.x, x0.y), S0);
+          S0 = fma2(f2(b.z, b.w), f2(x0.z, x0.w), S0);
+          S1 = fma2(f2(b.x, b.y), f2(x1.x, x1.y), S1);
+          S1 = fma2(f2(b.z, b.w), f2(x1.z, x1.w), S1);
         }
         const float* b3 = st_bs + lc * kRow + h3;
         const float* m3r = st_mv + m3 * kRow + h3;
@@ -411,12 +473,13 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
         for (int kk = 0; kk < 16; kk += 4) {
           const float4 b = *reinterpret_cast<const float4*>(b3 + kk);
           const float4 x2 = *reinterpret_cast<const float4*>(m3r + kk);
-          s2 = fmaf(b.x, x2.x, s2); s2 = fmaf(b.y, x2.y, s2);
-          s2 = fmaf(b.z, x2.z, s2); s2 = fmaf(b.w, x2.w, s2);
+          S2 = fma2(f2(b.x, b.y), f2(x2.x, x2.y), S2);
+          S2 = fma2(f2(b.z, b.w), f2(x2.z, x2.w), S2);
         }
+        float s2 = S2.x + S2.y;
         s2 += __shfl_xor_sync(0xffffffffu, s2, 16);
-        pv0[kmain] += s0;
-        pv1[kmain] += s1;
+        pv0[kmain] += S0.x + S0.y;
+        pv1[kmain] += S1.x + S1.y;
         if (third) pv2[kmain] += s2;
       }
       __syncwarp();
@@ -424,33 +487,50 @@ __global__ void __launch_bounds__(256, MINB) fused_f32(const __grid_constant__ P
     if (anchored) patch_flush<PX>(a, patch, pi0, pj0, pk0, lane);
     __syncwarp();
   }
-  if (worst != ST_OK) atomicMax(a.status, worst);
 }
 
-// Per-cell coefficient records (computed in f64, rounded once to f32):
-// float4 2m = (c0, c1, c2, c4), 2m+1 = (c3, c5, c6, c7) of component m
-// (Ex Ey Ez Bx By Bz).
+// Per-cell coefficient records (computed in f64, rounded once to f32), three
+// component pairs (a, b) = (Ex, Ey), (Bx, By), (Ez, Bz), four float4 each:
+// (c0a c0b c1a c1b) (c2a c2b c4a c4b) (c3a c3b c5a c5b) (c6a c6b c7a c7b).
 template <typename F>
 __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int nx, int ny,
                            int nz, float4* __restrict__ rec) {
   const int NY = ny + 1, NZ = nz + 1, NN = (nx + 1) * NY * NZ;
   const int ncell = nx * ny * nz;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
-    const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+  // component of pair slot (pair p, member h): Ex Ey | Bx By | Ez Bz
+  const int comp[6] = {0, 1, 3, 4, 2, 5};
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += gridDim.x * blockDim.x) {
+    // threads walk the cells k fastest (coalesced field reads, k is the
+    // fastest index of E / B); records are stored x fastest (sort order)
+    const int k = t % nz, j = (t / nz) % ny, i = t / (nz * ny);
+    const int c = i + nx * (j + ny * k);
     const int n0 = (i * NY + j) * NZ + k;
     const int sx = NY * NZ, sy = NZ;
+    float co[6][8];
 #pragma unroll
-    for (int m = 0; m < 6; ++m) {
+    for (int h = 0; h < 6; ++h) {
+      const int m = comp[h];
       const F* f = (m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN) + n0;
       const double f000 = f[0], f100 = f[sx], f010 = f[sy], f110 = f[sx + sy];
       const double f001 = f[1], f101 = f[sx + 1], f011 = f[sy + 1], f111 = f[sx + sy + 1];
-      const double c1 = f100 - f000, c2 = f010 - f000, c3 = f001 - f000;
-      const double c4 = (f110 - f100) - (f010 - f000);
-      const double c5 = (f101 - f001) - (f100 - f000);
-      const double c6 = (f011 - f001) - (f010 - f000);
-      const double c7 = ((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000));
-      rec[(size_t)c * 12 + 2 * m] = make_float4((float)f000, (float)c1, (float)c2, (float)c4);
-      rec[(size_t)c * 12 + 2 * m + 1] = make_float4((float)c3, (float)c5, (float)c6, (float)c7);
+      co[h][0] = (float)f000;
+      co[h][1] = (float)(f100 - f000);
+      co[h][2] = (float)(f010 - f000);
+      co[h][3] = (float)(f001 - f000);
+      co[h][4] = (float)((f110 - f100) - (f010 - f000));
+      co[h][5] = (float)((f101 - f001) - (f100 - f000));
+      co[h][6] = (float)((f011 - f001) - (f010 - f000));
+      co[h][7] = (float)(((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000)));
+    }
+    float4* o = rec + (size_t)c * 12;
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {
+      const float* A = co[2 * pr];
+      const float* Bq = co[2 * pr + 1];
+      o[4 * pr + 0] = make_float4(A[0], Bq[0], A[1], Bq[1]);
+      o[4 * pr + 1] = make_float4(A[2], Bq[2], A[4], Bq[4]);
+      o[4 * pr + 2] = make_float4(A[3], Bq[3], A[5], Bq[5]);
+      o[4 * pr + 3] = make_float4(A[6], Bq[6], A[7], Bq[7]);
     }
   }
 }
@@ -459,12 +539,61 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
 
 namespace {
 
-// kernel shape: patch width, chunk, blocks per SM (BP_F32_CFG=0/1 picks one)
-template <bool RX, bool RY, bool RZ, int PX, int CHUNK, int MINB>
-int launch_cfg(const f32k::Params& a, cudaStream_t s) {
-  auto k = f32k::fused_f32<RX, RY, RZ, PX, CHUNK, MINB>;
-  const size_t smem =
-      (size_t)(256 / 32) * (f32k::kStage + f32k::Patch<PX>::kFloats) * sizeof(float);
+int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+int sm_count_f32() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+int launch_mover_cfg(const f32k::Params& a, cudaStream_t s) {
+  auto k = f32k::mover_f32<RX, RY, RZ, REUSE, MINB>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  const long long need = (a.count + 255) / 256;
+  long long g = (long long)sm_count_f32() * per_sm;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(int)g, 256, 0, s>>>(a);
+  note_launch();
+  return launch_check("f32 mover launch");
+}
+
+template <bool RX, bool RY, bool RZ>
+int launch_mover(const f32k::Params& a, cudaStream_t s) {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* env = getenv("BP_F32_MOVER");
+    cfg = env ? atoi(env) : 0;
+  }
+  // record reuse across the mover iterations (the midpoint rarely leaves its
+  // cell) needs ~100 registers: 16 warps / SM; measured best on the GEM bench
+  switch (cfg) {
+    case 1: return launch_mover_cfg<RX, RY, RZ, false, 4>(a, s);
+    case 2: return launch_mover_cfg<RX, RY, RZ, false, 3>(a, s);
+    case 3: return launch_mover_cfg<RX, RY, RZ, true, 3>(a, s);
+    default: return launch_mover_cfg<RX, RY, RZ, true, 2>(a, s);
+  }
+}
+
+template <int PX, int CHUNK, int MINB>
+int launch_deposit_cfg(const f32k::Params& a, cudaStream_t s) {
+  auto k = f32k::deposit_f32<PX, CHUNK, MINB>;
+  const size_t smem = (size_t)(256 / 32) * (f32k::kStage + f32k::Patch<PX>::kFloats) * sizeof(float);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -473,32 +602,26 @@ int launch_cfg(const f32k::Params& a, cudaStream_t s) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
   if (per_sm < 1) per_sm = 1;
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long need = (a.count + 255) / 256;
-  long long g = (long long)sms * per_sm;
+  const long long need = (a.count + CHUNK * 8 - 1) / (CHUNK * 8);
+  long long g = (long long)sm_count_f32() * per_sm;
   if (need < g) g = need;
   if (g < 1) g = 1;
   k<<<(int)g, 256, smem, s>>>(a);
   note_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error("f32 fused kernel launch: %s", cudaGetErrorString(e));
-    return -2;
-  }
-  return 0;
+  return launch_check("f32 deposit launch");
 }
 
-template <bool RX, bool RY, bool RZ>
-int launch_bc(const f32k::Params& a, cudaStream_t s) {
+int launch_deposit(const f32k::Params& a, cudaStream_t s) {
   static int cfg = -1;
   if (cfg < 0) {
-    const char* env = getenv("BP_F32_CFG");
+    const char* env = getenv("BP_F32_DEPOSIT");
     cfg = env ? atoi(env) : 0;
   }
-  if (cfg == 1) return launch_cfg<RX, RY, RZ, 12, 1024, 2>(a, s);
-  return launch_cfg<RX, RY, RZ, 8, 512, 3>(a, s);
+  switch (cfg) {
+    case 1: return launch_deposit_cfg<8, 512, 2>(a, s);
+    case 2: return launch_deposit_cfg<12, 1024, 2>(a, s);
+    default: return launch_deposit_cfg<8, 512, 3>(a, s);
+  }
 }
 
 }  // namespace
@@ -560,33 +683,36 @@ int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
   a.status = c.status;
   void* rec = const_cast<void*>(rec_in);
   const size_t rbytes = f32_records_bytes(c.geo_i);
+  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 255) & ~(size_t)255;
   void* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, (rec ? 0 : rbytes) + 256, s);
+  cudaError_t e = cudaMallocAsync(&scratch, 256 + skip_bytes + (rec ? 0 : rbytes), s);
   if (e != cudaSuccess) {
     set_error("f32 scratch alloc: %s", cudaGetErrorString(e));
     return -2;
   }
   a.work = (unsigned long long*)scratch;
-  cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), s);
+  a.skip = (unsigned*)((char*)scratch + 256);
+  cudaMemsetAsync(scratch, 0, 256 + skip_bytes, s);
   int rc = 0;
   if (!rec) {
-    rec = (char*)scratch + 256;
+    rec = (char*)scratch + 256 + skip_bytes;
     rc = f32_pack_records(c.fbytes, c.E, c.B, c.geo_i, rec, s);
   }
   a.rec = (const float4*)rec;
   if (!rc) {
     const int m = (c.geo_i[3] ? 1 : 0) | (c.geo_i[4] ? 2 : 0) | (c.geo_i[5] ? 4 : 0);
     switch (m) {
-      case 0: rc = launch_bc<false, false, false>(a, s); break;
-      case 1: rc = launch_bc<true, false, false>(a, s); break;
-      case 2: rc = launch_bc<false, true, false>(a, s); break;
-      case 3: rc = launch_bc<true, true, false>(a, s); break;
-      case 4: rc = launch_bc<false, false, true>(a, s); break;
-      case 5: rc = launch_bc<true, false, true>(a, s); break;
-      case 6: rc = launch_bc<false, true, true>(a, s); break;
-      default: rc = launch_bc<true, true, true>(a, s); break;
+      case 0: rc = launch_mover<false, false, false>(a, s); break;
+      case 1: rc = launch_mover<true, false, false>(a, s); break;
+      case 2: rc = launch_mover<false, true, false>(a, s); break;
+      case 3: rc = launch_mover<true, true, false>(a, s); break;
+      case 4: rc = launch_mover<false, false, true>(a, s); break;
+      case 5: rc = launch_mover<true, false, true>(a, s); break;
+      case 6: rc = launch_mover<false, true, true>(a, s); break;
+      default: rc = launch_mover<true, true, true>(a, s); break;
     }
   }
+  if (!rc) rc = launch_deposit(a, s);
   cudaFreeAsync(scratch, s);
   return rc;
 }

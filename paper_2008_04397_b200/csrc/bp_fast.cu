@@ -26,7 +26,7 @@ int launch_fast(const Call& c, cudaStream_t s) {
   // selects the generic policy kernel instead, for comparisons)
   if (c.op == OP_FUSED && c.pbytes == 4) {
     const char* env = getenv("BP_F32_GENERIC");
-    if (!(env && env[0] == '1')) return f32_fused(c, nullptr, s);
+    if (!(env && env[0] == '1')) return f32_fused(c, c.records, s);
   }
   if (c.pbytes == 8 && c.fbytes == 8) return dispatch<double, double>(c, s);
   if (c.pbytes == 4 && c.fbytes == 4) return dispatch<float, float>(c, s);

@@ -25,6 +25,7 @@ struct Call {
   int n_iters, mixed, apply_bc;
   void* out;    // gather rows
   int* status;  // device int, atomicMax
+  const void* records;  // prebuilt f32 cell records (bp_field_records_build) or NULL
 };
 
 // Return 0 on a successful enqueue, else a negative BP_E* code.

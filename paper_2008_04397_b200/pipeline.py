@@ -115,6 +115,14 @@ class DeviceSimulation:
         self.mixed = 1 if npd != nfd else 0
         self.scale = float(nfd(MOMENT_SCALE))
         self._arith = {"parity": _lib.ARITH_PARITY, "fast": _lib.ARITH_FAST}[self.arith]
+        # f32 fast path: per-cell field records built once per field update
+        # (bp_field_records_build) and shared by every species' call
+        self.records = None
+        self._records_fresh = False
+        if self.arith == "fast" and pd == torch.float32:
+            gi = np.ascontiguousarray(self.geo_i, np.int64)
+            nbytes = int(_lib.load().bp_field_records_bytes(ctypes.c_void_p(gi.ctypes.data)))
+            self.records = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=self.device)
         if self.distributed:
             import torch.distributed as dist
             self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
@@ -153,6 +161,25 @@ class DeviceSimulation:
             self.B.copy_(self.torch.from_numpy(np.ascontiguousarray(B)), non_blocking=False)
         if self.distributed:
             broadcast_fields(self.E, self.B, src=0, group=self.group)
+        self._records_fresh = False
+
+    def _records_ptr(self, stream):
+        """Device address of the cell records for the current E/B (built on
+        first use after a field update), or None off the f32 fast path."""
+        if self.records is None:
+            return None
+        base = self.records.data_ptr()
+        ptr = (base + 255) & ~255
+        if not self._records_fresh:
+            L = _lib.load()
+            gi = np.ascontiguousarray(self.geo_i, np.int64)
+            rc = L.bp_field_records_build(self.E.element_size(), ctypes.c_void_p(self.E.data_ptr()),
+                                          ctypes.c_void_p(self.B.data_ptr()),
+                                          ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
+                                          ctypes.c_void_p(stream.cuda_stream))
+            _lib.check(rc, "field_records_build")
+            self._records_fresh = True
+        return ptr
 
     def _fused(self, sid, start, count, stream):
         p = self.particles[sid]
@@ -160,13 +187,15 @@ class DeviceSimulation:
         L = _lib.load()
         ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         hp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
-        rc = L.bp_fused_span_ex(
+        rec = self._records_ptr(stream)
+        rc = L.bp_fused_span_rec(
             self._arith, p.x.element_size(), self.E.element_size(),
             *[ptr(a) for a in p.arrays()], int(start), int(count), ptr(self.E), ptr(self.B),
             ptr(self.acc[sid]), ptr(self.invvol), hp(self.geo_f), hp(self.geo_g),
             hp(self.geo_i), float(sc["dt"]), float(sc["dth"]), float(sc["qdt2m"]),
             float(sc["beta"]), float(sc["one"]), int(self.species[sid].mover_iters),
-            self.scale, self.mixed, ptr(self.status), ctypes.c_void_p(stream.cuda_stream))
+            self.scale, self.mixed, None if rec is None else ctypes.c_void_p(rec),
+            ptr(self.status), ctypes.c_void_p(stream.cuda_stream))
         _lib.check(rc, "fused_span")
 
     def phase3(self, reduce=True):
@@ -265,6 +294,9 @@ class DeviceSimulation:
         torch = self.torch
         if E is not None or B is not None or self.distributed:
             self.set_fields(E, B)
+        # phase 1 always refreshes the cell records (a cycle's fields are new
+        # in a real run, even when the caller updated self.E / self.B in place)
+        self._records_fresh = False
         p3, kt = self.phase3()
         self.fold_moments()
         sort_ms, sorted_now = 0.0, False

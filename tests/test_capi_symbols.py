@@ -10,7 +10,7 @@ from conftest import ROOT
 
 def _declared():
     text = open(os.path.join(ROOT, "include", "bp_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(bp_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|long long|const char\*)\s+(bp_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
