@@ -47,6 +47,10 @@ sys.path.insert(0, ROOT)
 METRIC = ("particles moved+interpolated/sec (GEM 3D) at 1/2/4/8 B200; HBM GB/s fraction")
 UNIT = "particles/s"
 BYTES_PER_PARTICLE = {"single": 52, "mixed": 52, "double": 104}  # 13 words, SURVEY §8d
+# algorithmic words per particle of each kernel of the f32 fast path
+# (bp_f32.cu): the mover reads and writes x y z u v w, the deposit reads
+# x y z u v w q
+KERNEL_WORDS = {"mover": 12, "deposit": 7, "span": 13}
 
 
 def parse():
@@ -88,12 +92,12 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the fused kernel from the committed ncu
-    capture summary (profiles/ncu_summary_r01.json), or None."""
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    summary (profiles/ncu_summary_r01.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) as f:
-            return float(json.load(f)["span_kernel"]["dram_bytes_per_launch"])
+            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
     except Exception:
         return None
 
@@ -277,6 +281,8 @@ def main_ours(args):
     barrier()
     torch.cuda.synchronize()
     launches0 = L.bp_kernel_launches()
+    L.bp_timing_enable(1)
+    _lib.timing_read()  # discard anything recorded before the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     timed = []
     with ClockMonitor(local_dev) as mon:
@@ -286,6 +292,8 @@ def main_ours(args):
         e1.record()
         torch.cuda.synchronize()
     barrier()
+    ktimes = _lib.timing_read()
+    L.bp_timing_enable(0)
     launches = L.bp_kernel_launches() - launches0
     elapsed = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     kern = torch.tensor([sum(t.kernel_ms for t in timed)], dtype=torch.float64, device=dev)
@@ -296,22 +304,43 @@ def main_ours(args):
     elapsed_ms, kern_ms, sort_ms = float(elapsed), float(kern), float(sortms)
     value = n_total * args.steps / (elapsed_ms * 1e-3)
 
-    # roofline of the dominant kernel: one fused launch = one species' shard
+    # roofline of the dominant kernel (largest device time in the timed
+    # region, CUDA events on its launch stream): algorithmic bytes per launch
+    # (KERNEL_WORDS x word size x the launch's particles) / mean launch time
     hbm, peak_kind = peaks()
-    bpp = BYTES_PER_PARTICLE[args.precision]
+    word = BYTES_PER_PARTICLE[args.precision] // 13
     per_launch_particles = n_local / len(species)
-    launch_ms = kern_ms / (args.steps * len(species))
-    achieved = per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9
-    # the committed ncu capture is of the default 1-GPU C3 launch
-    traffic = ncu_traffic() if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
-                                and args.precision == "single" and args.arith == "fast") else None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
+    kinfo = {}
+    for k, (ms, cnt) in ktimes.items():
+        if cnt and k in KERNEL_WORDS:
+            lm = ms / cnt
+            ab = per_launch_particles * KERNEL_WORDS[k] * word
+            kinfo[k] = {"launches": cnt, "ms_per_launch": lm,
+                        "algorithmic_bytes_per_launch": ab,
+                        "achieved_gbs": ab / (lm * 1e-3) / 1e9,
+                        "frac": ab / (lm * 1e-3) / 1e9 / hbm,
+                        "share_of_step": ms / elapsed_ms}
+    dom = max(kinfo, key=lambda k: kinfo[k]["ms_per_launch"] * kinfo[k]["launches"])
+    dk = kinfo[dom]
+    names = {"mover": "bp::f32k::mover_f32 (implicit mover, 3 iterations)",
+             "deposit": "bp::f32k::deposit_f32 (10-moment interpolation)",
+             "span": "bp::span_kernel (generic fused mover + deposit)"}
+    traffic = ncu_traffic(dom) if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
+                                   and args.precision == "single"
+                                   and args.arith == "fast") else None
+    roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": dk["frac"], "traffic": traffic,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs copy)",
-                "kernel": "bp::span_kernel<FastPolicy<float,float>,fused> (+ per-call node "
-                          "record pack, timed together)",
-                "algorithmic_bytes_per_launch": per_launch_particles * bpp,
-                "launch_ms": launch_ms}
+                "kernel": names[dom],
+                "algorithmic_bytes_per_launch": dk["algorithmic_bytes_per_launch"],
+                "launch_ms": dk["ms_per_launch"], "kernels": kinfo}
+    # the whole fused phase against the north star's 13 words per particle
+    bpp = BYTES_PER_PARTICLE[args.precision]
+    launch_ms = kern_ms / (args.steps * len(species))
+    roofline["fused_phase"] = {
+        "ms_per_species": launch_ms,
+        "achieved_gbs": per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9,
+        "frac": per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9 / hbm}
 
     extra = {"phase3_kernel_ms_per_step": kern_ms / args.steps,
              "sort_ms_per_sort": sort_ms / max(1, sum(t.sorted_this_cycle for t in timed)),

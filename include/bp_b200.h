@@ -76,6 +76,15 @@ const char* bp_last_error(void);
  * threads): the evidence behind a benchmark's "gpu_launches". */
 long long bp_kernel_launches(void);
 
+/* Device timing of this library's kernels (benchmark evidence): while
+ * enabled, every mover / deposit / record-build / generic span launch is
+ * bracketed by CUDA events on its stream.  bp_timing_read() waits for them
+ * and returns per class (0 mover, 1 deposit, 2 record build, 3 generic span
+ * kernel) the summed milliseconds and launch counts since the last read,
+ * then resets; returns the number of classes. */
+int bp_timing_enable(int on);
+int bp_timing_read(double* ms, long long* counts, int n);
+
 /* Replaces kernels.fused_span (kernels.py:458-735): implicit mover with
  * boundary folding, then deposition of the 10 moments at the new state. */
 int bp_fused_span(int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us, void* vs,

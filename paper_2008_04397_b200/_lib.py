@@ -29,6 +29,7 @@ EXPORTS = (
     "bp_fused_span_host", "bp_sort_by_cell", "bp_sort_by_cell_into", "bp_cell_keys",
     "bp_fold_periodic_i64", "bp_moments_total", "bp_susceptibility",
     "bp_field_records_bytes", "bp_field_records_build", "bp_fused_span_rec",
+    "bp_timing_enable", "bp_timing_read",
 )
 
 _P = ctypes.c_void_p
@@ -49,6 +50,8 @@ _SIGS = {
                           + [_P] * 4 + [_P, _P, _P] + [_D] * 5
                           + [_INT, _D, _INT, _P, _P, _P]),
     "bp_field_records_bytes": (_I64, [_P]),
+    "bp_timing_enable": (_INT, [_INT]),
+    "bp_timing_read": (_INT, [_P, _P, _INT]),
     "bp_field_records_build": (_INT, [_INT, _P, _P, _P, _P, _P]),
     "bp_push_span": (_INT, [_INT, _INT] + [_P] * 6 + [_I64, _I64, _P, _P]
                      + [_P, _P, _P] + [_D] * 5 + [_INT, _INT, _INT, _P, _P]),
@@ -90,6 +93,18 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+TIMED_KERNELS = ("mover", "deposit", "records", "span")
+
+
+def timing_read():
+    """{class: (ms, launches)} of the library's timed kernels since the last
+    read (bp_timing_enable(1) first)."""
+    ms = (ctypes.c_double * len(TIMED_KERNELS))()
+    cnt = (ctypes.c_longlong * len(TIMED_KERNELS))()
+    load().bp_timing_read(ms, cnt, len(TIMED_KERNELS))
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(TIMED_KERNELS)}
 
 
 def last_error():

@@ -18,6 +18,48 @@ static std::atomic<long long> g_launches{0};
 
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Optional device timing per kernel class (bp_timing_enable / bp_timing_read):
+// an event pair on the launching stream around each launch, resolved when
+// the caller reads the totals.
+namespace {
+struct TimedSpan {
+  int cls;
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+std::atomic<bool> g_timing{false};
+std::vector<TimedSpan> g_spans;
+std::vector<cudaEvent_t> g_free_events;
+double g_tms[TK_COUNT] = {};
+long long g_tcnt[TK_COUNT] = {};
+
+cudaEvent_t take_event() {
+  if (!g_free_events.empty()) {
+    cudaEvent_t e = g_free_events.back();
+    g_free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+int timing_begin(int cls, cudaStream_t s) {
+  if (!g_timing.load(std::memory_order_relaxed)) return -1;
+  std::lock_guard<std::mutex> lock(g_tmu);
+  TimedSpan t{cls, take_event(), take_event()};
+  cudaEventRecord(t.a, s);
+  g_spans.push_back(t);
+  return (int)g_spans.size() - 1;
+}
+
+void timing_end(int idx, cudaStream_t s) {
+  if (idx < 0) return;
+  std::lock_guard<std::mutex> lock(g_tmu);
+  if (idx < (int)g_spans.size()) cudaEventRecord(g_spans[idx].b, s);
+}
+
 // Scratch (node records, sort buffers) comes from the device's default
 // stream-ordered pool; keep its memory mapped between calls instead of
 // returning it to the driver at every synchronisation (release threshold 0
@@ -257,6 +299,35 @@ using namespace bp;
 extern "C" {
 
 int bp_version(void) { return 100; }
+
+int bp_timing_enable(int on) {
+  std::lock_guard<std::mutex> lock(g_tmu);
+  g_timing.store(on != 0);
+  return BP_OK;
+}
+
+int bp_timing_read(double* ms, long long* counts, int n) {
+  std::lock_guard<std::mutex> lock(g_tmu);
+  for (auto& t : g_spans) {
+    float v = 0.f;
+    if (cudaEventSynchronize(t.b) == cudaSuccess && cudaEventElapsedTime(&v, t.a, t.b) == cudaSuccess) {
+      g_tms[t.cls] += v;
+      g_tcnt[t.cls] += 1;
+    }
+    g_free_events.push_back(t.a);
+    g_free_events.push_back(t.b);
+  }
+  g_spans.clear();
+  for (int k = 0; k < n && k < TK_COUNT; ++k) {
+    if (ms) ms[k] = g_tms[k];
+    if (counts) counts[k] = g_tcnt[k];
+  }
+  for (int k = 0; k < TK_COUNT; ++k) {
+    g_tms[k] = 0.0;
+    g_tcnt[k] = 0;
+  }
+  return TK_COUNT;
+}
 
 long long bp_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

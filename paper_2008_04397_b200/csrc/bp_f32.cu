@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ P
 // Deposit (interpolation of the 10 moments) of the moved particles.  Each
 // warp claims chunks of CHUNK particles; tiles of 32 are staged in shared
 // memory and folded per cell (see the comment above Patch).
-template <int PX, int CHUNK, int MINB>
+template <int PX, int CHUNK, int MINB, bool STRAY_VEC, bool STRAY_GROUP>
 __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__ Params a) {
   typedef Patch<PX> Pt;
   extern __shared__ float smem_f[];
@@ -397,23 +397,66 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
       const int kmain = useb ? kb : ka;
       const unsigned Mm = useb ? MB : MA;
       __syncwarp();
-      // ---- other cells of the tile: per-cell fold of their few particles
+      // ---- other cells of the tile.  A large group (a sorted run's next
+      // cell) is folded over its quads with the other lanes masked; the
+      // remaining strays are added one by one straight into the patch.
       unsigned rest = F & ~Mm;
-      while (rest) {
+      if (rest) {
         const int k2 = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
         const unsigned M2 = __ballot_sync(0xffffffffu, fit && pnode == k2);
-        rest &= ~M2;
-        float t0s = 0.f, t1s = 0.f, t2s = 0.f;
-        for (unsigned m = M2; m; m &= m - 1u) {
-          const int kk = __ffs(m) - 1;
-          const float b = st_bs[lc * kRow + kk];
-          t0s = fmaf(b, st_mv[lg * kRow + kk], t0s);
-          t1s = fmaf(b, st_mv[(lg + 4) * kRow + kk], t1s);
-          t2s = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], t2s);
+        const int q0 = (__ffs(M2) - 1) >> 2, q1 = (31 - __clz(M2)) >> 2;
+        if (STRAY_VEC && 20 * (q1 - q0 + 1) < 15 * __popc(M2)) {
+          rest &= ~M2;
+          F2 T0 = f2(0.f, 0.f), T1 = f2(0.f, 0.f), T2 = f2(0.f, 0.f);
+          const float* m2r = st_mv + (third ? lg + 8 : 8) * kRow;
+          for (int q = q0; q <= q1; ++q) {
+            const unsigned bits = M2 >> (4 * q);
+            float4 b = *reinterpret_cast<const float4*>(st_bs + lc * kRow + 4 * q);
+            b.x = (bits & 1u) ? b.x : 0.f;
+            b.y = (bits & 2u) ? b.y : 0.f;
+            b.z = (bits & 4u) ? b.z : 0.f;
+            b.w = (bits & 8u) ? b.w : 0.f;
+            const float4 x0 = *reinterpret_cast<const float4*>(st_mv + lg * kRow + 4 * q);
+            const float4 x1 = *reinterpret_cast<const float4*>(st_mv + (lg + 4) * kRow + 4 * q);
+            const float4 x2 = *reinterpret_cast<const float4*>(m2r + 4 * q);
+            T0 = fma2(f2(b.x, b.y), f2(x0.x, x0.y), T0);
+            T0 = fma2(f2(b.z, b.w), f2(x0.z, x0.w), T0);
+            T1 = fma2(f2(b.x, b.y), f2(x1.x, x1.y), T1);
+            T1 = fma2(f2(b.z, b.w), f2(x1.z, x1.w), T1);
+            T2 = fma2(f2(b.x, b.y), f2(x2.x, x2.y), T2);
+            T2 = fma2(f2(b.z, b.w), f2(x2.z, x2.w), T2);
+          }
+          pv0[k2] += T0.x + T0.y;
+          pv1[k2] += T1.x + T1.y;
+          if (third) pv2[k2] += T2.x + T2.y;
         }
-        pv0[k2] += t0s;
-        pv1[k2] += t1s;
-        if (third) pv2[k2] += t2s;
+        if (STRAY_GROUP) {
+          while (rest) {
+            const int kg = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
+            const unsigned MG = __ballot_sync(0xffffffffu, fit && pnode == kg);
+            rest &= ~MG;
+            float t0s = 0.f, t1s = 0.f, t2s = 0.f;
+            for (unsigned m = MG; m; m &= m - 1u) {
+              const int kk = __ffs(m) - 1;
+              const float b = st_bs[lc * kRow + kk];
+              t0s = fmaf(b, st_mv[lg * kRow + kk], t0s);
+              t1s = fmaf(b, st_mv[(lg + 4) * kRow + kk], t1s);
+              t2s = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], t2s);
+            }
+            pv0[kg] += t0s;
+            pv1[kg] += t1s;
+            if (third) pv2[kg] += t2s;
+          }
+        } else {
+          for (; rest; rest &= rest - 1u) {
+            const int kk = __ffs(rest) - 1;
+            const int k3 = __shfl_sync(0xffffffffu, pnode, kk);
+            const float b = st_bs[lc * kRow + kk];
+            pv0[k3] = fmaf(b, st_mv[lg * kRow + kk], pv0[k3]);
+            pv1[k3] = fmaf(b, st_mv[(lg + 4) * kRow + kk], pv1[k3]);
+            if (third) pv2[k3] = fmaf(b, st_mv[(lg + 8) * kRow + kk], pv2[k3]);
+          }
+        }
       }
       // ---- particles whose cells are outside the patch (rare): straight to the lattice
       unsigned out = V & ~F;
@@ -568,7 +611,9 @@ int launch_mover_cfg(const f32k::Params& a, cudaStream_t s) {
   long long g = (long long)sm_count_f32() * per_sm;
   if (need < g) g = need;
   if (g < 1) g = 1;
+  const int th = timing_begin(TK_MOVER, s);
   k<<<(int)g, 256, 0, s>>>(a);
+  timing_end(th, s);
   note_launch();
   return launch_check("f32 mover launch");
 }
@@ -590,9 +635,9 @@ int launch_mover(const f32k::Params& a, cudaStream_t s) {
   }
 }
 
-template <int PX, int CHUNK, int MINB>
+template <int PX, int CHUNK, int MINB, bool SV, bool SG>
 int launch_deposit_cfg(const f32k::Params& a, cudaStream_t s) {
-  auto k = f32k::deposit_f32<PX, CHUNK, MINB>;
+  auto k = f32k::deposit_f32<PX, CHUNK, MINB, SV, SG>;
   const size_t smem = (size_t)(256 / 32) * (f32k::kStage + f32k::Patch<PX>::kFloats) * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -606,7 +651,9 @@ int launch_deposit_cfg(const f32k::Params& a, cudaStream_t s) {
   long long g = (long long)sm_count_f32() * per_sm;
   if (need < g) g = need;
   if (g < 1) g = 1;
+  const int th = timing_begin(TK_DEPOSIT, s);
   k<<<(int)g, 256, smem, s>>>(a);
+  timing_end(th, s);
   note_launch();
   return launch_check("f32 deposit launch");
 }
@@ -618,9 +665,13 @@ int launch_deposit(const f32k::Params& a, cudaStream_t s) {
     cfg = env ? atoi(env) : 0;
   }
   switch (cfg) {
-    case 1: return launch_deposit_cfg<8, 512, 2>(a, s);
-    case 2: return launch_deposit_cfg<12, 1024, 2>(a, s);
-    default: return launch_deposit_cfg<8, 512, 3>(a, s);
+    // strays: per-cell groups folded then added (default, measured best on
+    // the GEM bench), + a masked-quad fold of a large second group, or one
+    // by one straight into the patch
+    case 1: return launch_deposit_cfg<8, 512, 3, true, true>(a, s);
+    case 2: return launch_deposit_cfg<8, 512, 3, false, false>(a, s);
+    case 3: return launch_deposit_cfg<12, 1024, 2, false, true>(a, s);
+    default: return launch_deposit_cfg<8, 512, 3, false, true>(a, s);
   }
 }
 
@@ -637,12 +688,14 @@ int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* ge
   const long long ncell = (long long)nx * ny * nz;
   int blocks = (int)((ncell + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
+  const int th = timing_begin(TK_RECORDS, s);
   if (fbytes == 8)
     f32k::pack_cells<double><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B, nx, ny,
                                                      nz, (float4*)rec);
   else
     f32k::pack_cells<float><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B, nx, ny, nz,
                                                     (float4*)rec);
+  timing_end(th, s);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -45,6 +45,11 @@ int f32_fused(const Call& c, const void* rec, cudaStream_t s);
 // count of kernels this library launched (bp_kernel_launches)
 void note_launch(int n = 1);
 
+// device timing per kernel class (bp_timing_*): begin returns a handle or -1
+enum { TK_MOVER = 0, TK_DEPOSIT = 1, TK_RECORDS = 2, TK_SPAN = 3, TK_COUNT = 4 };
+int timing_begin(int cls, cudaStream_t s);
+void timing_end(int handle, cudaStream_t s);
+
 // keep the default stream-ordered pool's memory mapped between calls
 void ensure_pool();
 

@@ -133,7 +133,9 @@ int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t c
   }
   // one wave of resident blocks; every warp walks a contiguous run of >= 32
   const int grid = grid_for(k, smem, count, kThreads);
+  const int th = timing_begin(TK_SPAN, s);
   k<<<grid, kThreads, smem, s>>>(a);
+  timing_end(th, s);
   note_launch();
   return launch_error("span kernel launch");
 }
