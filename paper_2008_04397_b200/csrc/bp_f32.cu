@@ -70,11 +70,18 @@ __device__ __forceinline__ float rcp_approx(float d) {
   return r;
 }
 
-// one 32-byte load (LDG.E.ENL2.256) into two float4
+// one 32-byte load (LDG.E.ENL2.256) into two float4; cell records are
+// kept in L1 / L2 in preference to the particle streams (evict_last)
 __device__ __forceinline__ void ldg8(const float4* p, float4& a, float4& b) {
-  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm("ld.global.nc.L1::evict_last.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
       : "l"(p));
+}
+
+// pull a cell record (192 bytes = two 128-byte lines) into L1
+__device__ __forceinline__ void prefetch_record(const float4* r) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(r));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(r + 11));
 }
 
 template <bool REFL>
@@ -252,25 +259,40 @@ __device__ __forceinline__ void patch_flush(const Params& a, float* patch, int p
 // the SM holds enough warps to hide the latency of the three dependent
 // gather + rotation steps.  Particles that fail (kernels.py:618-621, 672-676)
 // are not stored; their bit in `skip` keeps them out of the deposit.
-template <bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+template <bool RX, bool RY, bool RZ, bool REUSE, int MINB, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ Params a) {
-  // persistent grid: each thread walks particles r, r + stride, ... with the
-  // next particle's loads in flight while the current one is pushed
+  // persistent grid: each thread walks particles r, r + stride, ...; the
+  // loads of the particle two steps ahead are in flight, and the record of
+  // the next particle's cell is prefetched into L1 while this one is pushed
   const long long stride = (long long)gridDim.x * 256;
   long long r = (long long)blockIdx.x * 256 + threadIdx.x;
-  float nx_ = 0.f, ny_ = 0.f, nz_ = 0.f, nu_ = 0.f, nv_ = 0.f, nw_ = 0.f;
-  auto fetch = [&](long long rr) {
+  float n1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, n2[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto fetch = [&](long long rr, float* d) {
     if (rr < a.count) {
       const long long p = a.start + rr;
-      nx_ = __ldcs(a.x + p); ny_ = __ldcs(a.y + p); nz_ = __ldcs(a.z + p);
-      nu_ = __ldcs(a.u + p); nv_ = __ldcs(a.v + p); nw_ = __ldcs(a.w + p);
+      d[0] = __ldcs(a.x + p); d[1] = __ldcs(a.y + p); d[2] = __ldcs(a.z + p);
+      d[3] = __ldcs(a.u + p); d[4] = __ldcs(a.v + p); d[5] = __ldcs(a.w + p);
     }
   };
-  fetch(r);
+  fetch(r, n1);
+  if (PF) fetch(r + stride, n2);
   const long long rbase = r - (threadIdx.x & 31);  // warp-uniform loop bound
   for (long long rb = rbase; rb < a.count; rb += stride, r += stride) {
-    float xp = nx_, yp = ny_, zp = nz_, un = nu_, vn = nv_, wn = nw_;
-    fetch(r + stride);
+    float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
+    if (PF) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) n1[q] = n2[q];
+      fetch(r + 2 * stride, n2);
+      float fx, fy, fz;
+      int i, j, k;
+      const int cell = cell_of(a, n1[0], n1[1], n1[2], fx, fy, fz, i, j, k);
+      // one prefetch per distinct cell of the warp (sorted runs share cells)
+      const int prev = __shfl_up_sync(0xffffffffu, cell, 1);
+      if (r + stride < a.count && ((threadIdx.x & 31) == 0 || prev != cell))
+        prefetch_record(a.rec + (size_t)cell * 12);
+    } else {
+      fetch(r + stride, n1);
+    }
     int st = ST_OK;
     if (r < a.count) {
       const long long p = a.start + r;
@@ -292,7 +314,10 @@ __global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ P
 // Deposit (interpolation of the 10 moments) of the moved particles.  Each
 // warp claims chunks of CHUNK particles; tiles of 32 are staged in shared
 // memory and folded per cell (see the comment above Patch).
-template <int PX, int CHUNK, int MINB, bool STRAY_VEC, bool STRAY_GROUP>
+// PUSH: the fused variant (mover + deposit in one pass over the particles,
+// BC kinds RX RY RZ); otherwise the particles are deposited as they are.
+template <int PX, int CHUNK, int MINB, bool STRAY_VEC, int STRAY_GROUP, bool PUSH = false,
+          bool RX = false, bool RY = false, bool RZ = false>
 __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__ Params a) {
   typedef Patch<PX> Pt;
   extern __shared__ float smem_f[];
@@ -325,7 +350,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
       pu_ = __ldcs(a.u + p); pv_ = __ldcs(a.v + p); pw_ = __ldcs(a.w + p);
       pq_ = __ldcs(a.q + p);
     }
-    sk_ = __ldg(a.skip + (r >> 5));
+    if (!PUSH) sk_ = __ldg(a.skip + (r >> 5));
   };
   if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
   while (nxt < a.count) {
@@ -337,10 +362,22 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
     bool anchored = false;
     for (long long t0 = w0; t0 < w1; t0 += 32) {
       const long long r = t0 + lane;
-      const bool valid = r < w1 && !((sk_ >> lane) & 1u);
-      const float xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_, qp = pq_;
+      bool valid = r < w1 && (PUSH || !((sk_ >> lane) & 1u));
+      float xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_;
+      const float qp = pq_;
       if (t0 + 32 < w1) fetch(t0 + 32 + lane, w1);
       else if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
+      if (PUSH && valid) {
+        const int st = push<RX, RY, RZ, true>(a, xp, yp, zp, un, vn, wn);
+        if (st != ST_OK) {
+          atomicMax(a.status, st);  // not stored, not deposited (kernels.py:618-621)
+          valid = false;
+        } else {
+          const long long p = a.start + r;
+          __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
+          __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
+        }
+      }
       // ---- stage this lane's particle: 8 bases q*w_c and the moments
       int ci = 0, cj = 0, ck = 0;
       {
@@ -430,7 +467,47 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
           pv1[k2] += T1.x + T1.y;
           if (third) pv2[k2] += T2.x + T2.y;
         }
-        if (STRAY_GROUP) {
+        if (STRAY_GROUP == 2) {
+          // two cells per round: independent fold / update chains
+          while (rest) {
+            const int ka = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
+            const unsigned MA2 = __ballot_sync(0xffffffffu, fit && pnode == ka);
+            rest &= ~MA2;
+            const int kb2 = __shfl_sync(0xffffffffu, pnode, __ffs(rest | 0x80000000u) - 1);
+            const unsigned MB2 = rest ? __ballot_sync(0xffffffffu, fit && pnode == kb2) : 0u;
+            rest &= ~MB2;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+            unsigned ma = MA2, mb = MB2;
+            while (ma | mb) {
+              if (ma) {
+                const int kk = __ffs(ma) - 1;
+                ma &= ma - 1u;
+                const float b = st_bs[lc * kRow + kk];
+                a0 = fmaf(b, st_mv[lg * kRow + kk], a0);
+                a1 = fmaf(b, st_mv[(lg + 4) * kRow + kk], a1);
+                a2 = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], a2);
+              }
+              if (mb) {
+                const int kk = __ffs(mb) - 1;
+                mb &= mb - 1u;
+                const float b = st_bs[lc * kRow + kk];
+                b0 = fmaf(b, st_mv[lg * kRow + kk], b0);
+                b1 = fmaf(b, st_mv[(lg + 4) * kRow + kk], b1);
+                b2 = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], b2);
+              }
+            }
+            const float pa0 = pv0[ka], pa1 = pv1[ka];
+            if (MB2) {
+              const float pb0 = pv0[kb2], pb1 = pv1[kb2];
+              pv0[kb2] = pb0 + b0;
+              pv1[kb2] = pb1 + b1;
+              if (third) pv2[kb2] += b2;
+            }
+            pv0[ka] = pa0 + a0;
+            pv1[ka] = pa1 + a1;
+            if (third) pv2[ka] += a2;
+          }
+        } else if (STRAY_GROUP) {
           while (rest) {
             const int kg = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
             const unsigned MG = __ballot_sync(0xffffffffu, fit && pnode == kg);
@@ -601,9 +678,9 @@ int sm_count_f32() {
   return sms;
 }
 
-template <bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+template <bool RX, bool RY, bool RZ, bool REUSE, int MINB, bool PF = false>
 int launch_mover_cfg(const f32k::Params& a, cudaStream_t s) {
-  auto k = f32k::mover_f32<RX, RY, RZ, REUSE, MINB>;
+  auto k = f32k::mover_f32<RX, RY, RZ, REUSE, MINB, PF>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
   if (per_sm < 1) per_sm = 1;
@@ -628,16 +705,16 @@ int launch_mover(const f32k::Params& a, cudaStream_t s) {
   // record reuse across the mover iterations (the midpoint rarely leaves its
   // cell) needs ~100 registers: 16 warps / SM; measured best on the GEM bench
   switch (cfg) {
-    case 1: return launch_mover_cfg<RX, RY, RZ, false, 4>(a, s);
-    case 2: return launch_mover_cfg<RX, RY, RZ, false, 3>(a, s);
-    case 3: return launch_mover_cfg<RX, RY, RZ, true, 3>(a, s);
+    case 1: return launch_mover_cfg<RX, RY, RZ, true, 2, true>(a, s);  // + record prefetch
+    case 2: return launch_mover_cfg<RX, RY, RZ, true, 3>(a, s);
     default: return launch_mover_cfg<RX, RY, RZ, true, 2>(a, s);
   }
 }
 
-template <int PX, int CHUNK, int MINB, bool SV, bool SG>
+template <int PX, int CHUNK, int MINB, bool SV, int SG, bool PUSH = false, bool RX = false,
+          bool RY = false, bool RZ = false>
 int launch_deposit_cfg(const f32k::Params& a, cudaStream_t s) {
-  auto k = f32k::deposit_f32<PX, CHUNK, MINB, SV, SG>;
+  auto k = f32k::deposit_f32<PX, CHUNK, MINB, SV, SG, PUSH, RX, RY, RZ>;
   const size_t smem = (size_t)(256 / 32) * (f32k::kStage + f32k::Patch<PX>::kFloats) * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -668,10 +745,13 @@ int launch_deposit(const f32k::Params& a, cudaStream_t s) {
     // strays: per-cell groups folded then added (default, measured best on
     // the GEM bench), + a masked-quad fold of a large second group, or one
     // by one straight into the patch
-    case 1: return launch_deposit_cfg<8, 512, 3, true, true>(a, s);
-    case 2: return launch_deposit_cfg<8, 512, 3, false, false>(a, s);
-    case 3: return launch_deposit_cfg<12, 1024, 2, false, true>(a, s);
-    default: return launch_deposit_cfg<8, 512, 3, false, true>(a, s);
+    case 1: return launch_deposit_cfg<8, 512, 3, true, 1>(a, s);
+    case 2: return launch_deposit_cfg<8, 512, 3, false, 0>(a, s);
+    case 3: return launch_deposit_cfg<12, 1024, 2, false, 1>(a, s);
+    case 4: return launch_deposit_cfg<8, 512, 3, false, 2>(a, s);
+    case 5: return launch_deposit_cfg<8, 1024, 3, false, 1>(a, s);
+    case 6: return launch_deposit_cfg<8, 256, 3, false, 1>(a, s);
+    default: return launch_deposit_cfg<8, 512, 3, false, 1>(a, s);
   }
 }
 
@@ -752,6 +832,20 @@ int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
     rc = f32_pack_records(c.fbytes, c.E, c.B, c.geo_i, rec, s);
   }
   a.rec = (const float4*)rec;
+  static int fusedk = -1;
+  if (fusedk < 0) {
+    const char* env = getenv("BP_F32_FUSED");
+    fusedk = (env && env[0] == '1') ? 1 : 0;
+  }
+  if (!rc && fusedk) {
+    // one-pass variant (dev comparison): mover + deposit in one kernel
+    const int m = (c.geo_i[3] ? 1 : 0) | (c.geo_i[4] ? 2 : 0) | (c.geo_i[5] ? 4 : 0);
+    if (m == 2) rc = launch_deposit_cfg<8, 512, 2, false, 1, true, false, true, false>(a, s);
+    else if (m == 0) rc = launch_deposit_cfg<8, 512, 2, false, 1, true, false, false, false>(a, s);
+    else { set_error("fused f32 variant: only P/R/P and periodic boxes"); rc = -1; }
+    cudaFreeAsync(scratch, s);
+    return rc;
+  }
   if (!rc) {
     const int m = (c.geo_i[3] ? 1 : 0) | (c.geo_i[4] ? 2 : 0) | (c.geo_i[5] ? 4 : 0);
     switch (m) {

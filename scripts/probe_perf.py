@@ -38,8 +38,9 @@ v = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * vth).to(pd)
 w = (torch.randn(n, device=dev, generator=g, dtype=torch.float64) * vth).to(pd)
 q = torch.full((n,), -1e-4, device=dev, dtype=pd)
 shp = (3,) + geom.node_shape
-E = (torch.randn(shp, device=dev, generator=g, dtype=torch.float64) * 1e-3).to(fd)
-B = (torch.randn(shp, device=dev, generator=g, dtype=torch.float64) * 1e-2).to(fd)
+ebs = float(os.environ.get("PROBE_EB", "1"))
+E = (torch.randn(shp, device=dev, generator=g, dtype=torch.float64) * 1e-3 * ebs).to(fd)
+B = (torch.randn(shp, device=dev, generator=g, dtype=torch.float64) * 1e-2 * ebs).to(fd)
 inv = torch.from_numpy(geom.inv_node_volume(nfd)).to(dev)
 acc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device=dev)
 sp = SpeciesParams(0, -1.0, 1 / 64.0, ppc)
