@@ -80,12 +80,12 @@ def test_deposit_and_gather_match_reference_golden(gpu, mode, ci):
 
 
 def _random_state(mode, n, seed, cells=(16, 8, 8), box=(6.4, 3.2, 3.2), vscale=0.3,
-                  order="random"):
+                  order="random", bc=("periodic", "reflecting", "periodic")):
     from paper_2008_04397_b200.geometry import GridGeometry
     from paper_2008_04397_b200 import kernels as K
     from paper_2008_04397_b200.config import SpeciesParams
     pd, fd = MODES[mode]
-    geom = GridGeometry.from_box(cells, box, bc=("periodic", "reflecting", "periodic"))
+    geom = GridGeometry.from_box(cells, box, bc=bc)
     rng = np.random.default_rng(seed)
     x = rng.random(n) * geom.Lx
     y = rng.random(n) * geom.Ly
@@ -289,3 +289,50 @@ def test_fast_f32_fused_is_deterministic(gpu, mode):
     for dacc, d in outs[1:]:
         assert torch.equal(dacc, outs[0][0])
         assert all(torch.equal(a, b) for a, b in zip(d, outs[0][1]))
+
+
+_BCS = [(a, b, c) for a in ("periodic", "reflecting") for b in ("periodic", "reflecting")
+        for c in ("periodic", "reflecting")]
+
+
+@pytest.mark.parametrize("bc", _BCS, ids=["".join(k[0] for k in b) for b in _BCS])
+@pytest.mark.parametrize("failing", [False, True])
+def test_fast_f32_every_boundary_kind(gpu, oracle, bc, failing):
+    """The f32 kernels are instantiated per boundary kind (bp_f32.cu): every
+    combination against the oracle within 1e-4, on a span with an unaligned
+    start and a ragged tail.  `failing` gives one particle in 97 a velocity
+    of 1e4 (a certain runaway / midpoint failure): those must be neither
+    stored nor deposited, exactly as in the reference."""
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 60_013
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(
+        "single", n, seed=101, order="sorted", bc=bc)
+    if failing:
+        bad = np.arange(5, n, 97)
+        arrs[3][bad] = pd(1e4)
+        arrs[4][bad[::2]] = pd(-1e4)
+    inv = geom.inv_node_volume(fd)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+            fd(SCALE), 0)
+    start, count = 77, n - 77 - 5
+    ref = [a.copy() for a in arrs]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    st_ref = oracle.fused_span(*ref, start, count, E, B, acc_ref, inv, *tail)
+    d = _dev(torch, arrs)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    st = K.fused_span(*d, start, count, dE, dB, dacc, dinv, *tail, arith="fast")
+    assert st == st_ref
+    assert (st != 0) == failing
+    periods = [geom.lengths[k] if bc[k] == "periodic" else None for k in range(3)]
+    periods += [None, None, None]
+    for name, r, t, per in zip("xyzuvw", ref, d, periods):
+        got = t.cpu().numpy()
+        # outside the span nothing moves
+        assert np.array_equal(got[:start], r[:start]) and np.array_equal(got[start + count:],
+                                                                            r[start + count:])
+        _assert_close(name, r, got, 1e-4, per)
+    got = dacc.cpu().numpy()
+    for m in range(10):
+        _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, 1e-4)
