@@ -228,28 +228,51 @@ __device__ __forceinline__ long long lattice(const Params& a, float v, int node)
   return __double2ll_rn((double)v * iv * a.scale);
 }
 
-// Flush and clear the patch: each lane takes rows of 4 z-consecutive nodes.
+// The patch's nodes are split over the lanes (node lane + 32 i, i < PX/2);
+// each lane holds invvol * 2^43 of its nodes in registers, loaded when the
+// patch is anchored so the loads complete long before the flush uses them.
 template <int PX>
-__device__ __forceinline__ void patch_flush(const Params& a, float* patch, int pi0, int pj0,
-                                            int pk0, unsigned lane) {
-  typedef Patch<PX> Pt;
-  for (int r = lane; r < 10 * PX * 4; r += 32) {
-    const int m = r / (PX * 4), rr = r - m * (PX * 4);
-    const int px = rr >> 2, py = rr & 3;
-    float* row = patch + m * Pt::kStride + rr * 4;
-    const float2 v01 = *reinterpret_cast<const float2*>(row);
-    const float2 v23 = *reinterpret_cast<const float2*>(row + 2);
-    if (v01.x != 0.f || v01.y != 0.f || v23.x != 0.f || v23.y != 0.f) {
-      const int node = ((pi0 + px) * a.NY + (pj0 + py)) * a.NZ + pk0;
-      long long* dst = a.acc + (size_t)m * a.NN + node;
-      const float vv[4] = {v01.x, v01.y, v23.x, v23.y};
+struct PatchNodes {
+  static constexpr int kPer = PX * 16 / 32;
+  double ivs[kPer];
+  int gnode[kPer];  // global node index, -1 outside the grid
+};
+
+template <int PX>
+__device__ __forceinline__ void patch_anchor(const Params& a, PatchNodes<PX>& pn, int pi0,
+                                             int pj0, int pk0, unsigned lane) {
 #pragma unroll
-      for (int z = 0; z < 4; ++z)
-        if (vv[z] != 0.f)
-          atomicAdd(reinterpret_cast<unsigned long long*>(dst + z),
-                    (unsigned long long)lattice(a, vv[z], node + z));
-      *reinterpret_cast<float2*>(row) = make_float2(0.f, 0.f);
-      *reinterpret_cast<float2*>(row + 2) = make_float2(0.f, 0.f);
+  for (int i = 0; i < PatchNodes<PX>::kPer; ++i) {
+    const int n = (int)lane + 32 * i;
+    const int gi = pi0 + (n >> 4), gj = pj0 + ((n >> 2) & 3), gk = pk0 + (n & 3);
+    const bool in = gi >= 0 && gi <= a.nx && gj >= 0 && gj <= a.ny && gk >= 0 && gk <= a.nz;
+    const int g = in ? (gi * a.NY + gj) * a.NZ + gk : 0;
+    pn.gnode[i] = in ? g : -1;
+    const double iv = a.iv_d ? __ldg(a.iv_d + g) : (double)__ldg(a.iv_f + g);
+    pn.ivs[i] = iv * a.scale;
+  }
+}
+
+// Flush and clear the patch: lane handles its nodes for all 10 moments; a
+// nonzero sum goes onto the lattice (x invvol x 2^43, rint) with one
+// REDG.ADD.64 (consecutive lanes hold z-consecutive nodes).
+template <int PX>
+__device__ __forceinline__ void patch_flush(const Params& a, float* patch,
+                                            const PatchNodes<PX>& pn, unsigned lane) {
+  typedef Patch<PX> Pt;
+#pragma unroll
+  for (int i = 0; i < PatchNodes<PX>::kPer; ++i) {
+    const int n = (int)lane + 32 * i;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      float* pv = patch + m * Pt::kStride + n;
+      const float v = *pv;
+      if (v != 0.f) {
+        *pv = 0.f;
+        if (pn.gnode[i] >= 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)m * a.NN + pn.gnode[i]),
+                    (unsigned long long)__double2ll_rn((double)v * pn.ivs[i]));
+      }
     }
   }
 }
@@ -360,6 +383,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
     int pi0 = 0, pj0 = 0, pk0 = 0;  // patch origin (node coordinates)
     bool anchored = false;
+    PatchNodes<PX> pn;
     for (long long t0 = w0; t0 < w1; t0 += 32) {
       const long long r = t0 + lane;
       bool valid = r < w1 && (PUSH || !((sk_ >> lane) & 1u));
@@ -407,6 +431,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
         pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
         pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
         pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+        patch_anchor<PX>(a, pn, pi0, pj0, pk0, lane);
       }
       int dx = ci - pi0, dy = cj - pj0, dz = ck - pk0;
       bool fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
@@ -414,11 +439,12 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
       unsigned F = __ballot_sync(0xffffffffu, fit);
       if (__popc(V & ~F) > __popc(F)) {
         // the run moved on: flush and re-anchor at its first particle outside
-        patch_flush<PX>(a, patch, pi0, pj0, pk0, lane);
+        patch_flush<PX>(a, patch, pn, lane);
         const int src = __ffs(V & ~F) - 1;
         pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
         pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
         pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+        patch_anchor<PX>(a, pn, pi0, pj0, pk0, lane);
         dx = ci - pi0; dy = cj - pj0; dz = ck - pk0;
         fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
               (unsigned)dz <= 2u;
@@ -604,7 +630,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
       }
       __syncwarp();
     }
-    if (anchored) patch_flush<PX>(a, patch, pi0, pj0, pk0, lane);
+    if (anchored) patch_flush<PX>(a, patch, pn, lane);
     __syncwarp();
   }
 }
