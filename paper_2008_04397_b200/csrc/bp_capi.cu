@@ -234,12 +234,16 @@ int fused_call(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, 
 
 // ---------------------------------------------------------------------------
 // Host-memory streaming pipeline (bp_fused_span_host).
+constexpr int kSlots = 3;  // batches in flight: H2D of one, kernels, D2H of another
+
 struct HostCtx {
   int dev = -1;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t ready[2];
-  void* slot[2][7] = {};
+  cudaStream_t st[kSlots] = {};
+  cudaEvent_t ready[kSlots];
+  void* slot[kSlots][7] = {};
   size_t slot_bytes = 0;
+  void* rec = nullptr;  // f32 cell records, built once per call
+  size_t rec_bytes = 0;
   void* dE = nullptr;
   void* dB = nullptr;
   void* dinv = nullptr;
@@ -257,7 +261,7 @@ int host_ctx_reserve(HostCtx& h, size_t slot_bytes, size_t field_bytes, size_t a
   if (h.dev != dev) {
     h = HostCtx();
     h.dev = dev;
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kSlots; ++k) {
       if (cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&h.ready[k], cudaEventDisableTiming) != cudaSuccess)
         return cuda_check(cudaGetLastError(), "stream create");
@@ -267,7 +271,7 @@ int host_ctx_reserve(HostCtx& h, size_t slot_bytes, size_t field_bytes, size_t a
       return cuda_check(cudaGetLastError(), "status alloc");
   }
   if (slot_bytes > h.slot_bytes) {
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < kSlots; ++k)
       for (int a = 0; a < 7; ++a) {
         if (h.slot[k][a]) cudaFree(h.slot[k][a]);
         if (cudaMalloc(&h.slot[k][a], slot_bytes) != cudaSuccess)
@@ -492,7 +496,7 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
   std::lock_guard<std::mutex> lock(g_host_mu);
   HostCtx& h = g_host;
   const int64_t nn = (geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
-  int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 23);
+  int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 22);
   if (batch > count) batch = count;
   rc = host_ctx_reserve(h, (size_t)batch * pbytes, (size_t)3 * nn * fbytes,
                         (size_t)10 * nn * sizeof(int64_t));
@@ -504,13 +508,27 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
   rc |= cuda_check(cudaMemcpyAsync(h.dinv, invvol, nn * fbytes, cudaMemcpyHostToDevice, s0), "invvol h2d");
   rc |= cuda_check(cudaMemcpyAsync(h.dacc, acc, 10 * nn * 8, cudaMemcpyHostToDevice, s0), "acc h2d");
   rc |= cuda_check(cudaMemsetAsync(h.dstatus, 0, sizeof(int), s0), "status");
+  // f32 fast path: the cell records of E/B once for all batches
+  const bool f32rec = arith == BP_ARITH_FAST && pbytes == 4;
+  if (f32rec && !rc) {
+    const size_t rb = f32_records_bytes(geo_i) + 256;
+    if (rb > h.rec_bytes) {
+      if (h.rec) cudaFree(h.rec);
+      h.rec = nullptr;
+      h.rec_bytes = 0;
+      rc = cuda_check(cudaMalloc(&h.rec, rb), "records alloc");
+      if (!rc) h.rec_bytes = rb;
+    }
+    if (!rc) rc = f32_pack_records(fbytes, h.dE, h.dB, geo_i, h.rec, s0) ? BP_ECUDA : BP_OK;
+  }
   rc |= cuda_check(cudaEventRecord(h.ready[0], s0), "event");
-  if (rc) return BP_ECUDA;
-  rc |= cuda_check(cudaStreamWaitEvent(h.st[1], h.ready[0], 0), "wait");
+  if (rc) return rc < 0 ? rc : BP_ECUDA;
+  for (int k = 1; k < kSlots; ++k)
+    rc |= cuda_check(cudaStreamWaitEvent(h.st[k], h.ready[0], 0), "wait");
   char* host[7] = {(char*)xs, (char*)ys, (char*)zs, (char*)us, (char*)vs, (char*)ws, (char*)qs};
   int64_t b = 0;
   for (int64_t off = 0; off < count && !rc; off += batch, ++b) {
-    const int k = (int)(b & 1);
+    const int k = (int)(b % kSlots);
     cudaStream_t s = h.st[k];
     const int64_t n = (count - off < batch) ? count - off : batch;
     const size_t bytes = (size_t)n * pbytes;
@@ -530,15 +548,18 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
     c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
     c.n_iters = n_iters; c.mixed = mixed; c.apply_bc = 1;
     c.status = h.dstatus;
+    c.records = f32rec ? h.rec : nullptr;
     rc = arith == BP_ARITH_FAST ? launch_fast(c, s) : launch_parity(c, s);
     if (rc) break;
     for (int a = 0; a < 6 && !rc; ++a)
       rc = cuda_check(cudaMemcpyAsync(host[a] + hoff, h.slot[k][a], bytes,
                                       cudaMemcpyDeviceToHost, s), "batch d2h");
   }
-  // join both streams, bring the accumulator and status back
-  cudaEventRecord(h.ready[1], h.st[1]);
-  cudaStreamWaitEvent(s0, h.ready[1], 0);
+  // join the streams, bring the accumulator and status back
+  for (int k = 1; k < kSlots; ++k) {
+    cudaEventRecord(h.ready[k], h.st[k]);
+    cudaStreamWaitEvent(s0, h.ready[k], 0);
+  }
   if (!rc) rc = cuda_check(cudaMemcpyAsync(acc, h.dacc, 10 * nn * 8, cudaMemcpyDeviceToHost, s0), "acc d2h");
   if (!rc) rc = cuda_check(cudaMemcpyAsync(h.hstatus, h.dstatus, sizeof(int), cudaMemcpyDeviceToHost, s0), "status d2h");
   int rc2 = cuda_check(cudaStreamSynchronize(s0), "pipeline");

@@ -534,21 +534,28 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
             if (third) pv2[ka] += a2;
           }
         } else if (STRAY_GROUP) {
+          const float* brow = st_bs + lc * kRow;
+          const float* m0row = st_mv + lg * kRow;
+          const float* m1row = st_mv + (lg + 4) * kRow;
+          const float* m2row = st_mv + (third ? lg + 8 : 8) * kRow;
           while (rest) {
             const int kg = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
             const unsigned MG = __ballot_sync(0xffffffffu, fit && pnode == kg);
             rest &= ~MG;
+            // the cell's patch values are read first (no alias with the
+            // staged rows) so their latency hides behind the fold
+            const float o0 = pv0[kg], o1 = pv1[kg], o2 = pv2[kg];
             float t0s = 0.f, t1s = 0.f, t2s = 0.f;
             for (unsigned m = MG; m; m &= m - 1u) {
               const int kk = __ffs(m) - 1;
-              const float b = st_bs[lc * kRow + kk];
-              t0s = fmaf(b, st_mv[lg * kRow + kk], t0s);
-              t1s = fmaf(b, st_mv[(lg + 4) * kRow + kk], t1s);
-              t2s = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], t2s);
+              const float b = brow[kk];
+              t0s = fmaf(b, m0row[kk], t0s);
+              t1s = fmaf(b, m1row[kk], t1s);
+              t2s = fmaf(b, m2row[kk], t2s);
             }
-            pv0[kg] += t0s;
-            pv1[kg] += t1s;
-            if (third) pv2[kg] += t2s;
+            pv0[kg] = o0 + t0s;
+            pv1[kg] = o1 + t1s;
+            if (third) pv2[kg] = o2 + t2s;
           }
         } else {
           for (; rest; rest &= rest - 1u) {
