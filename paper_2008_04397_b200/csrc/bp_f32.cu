@@ -49,6 +49,8 @@ struct Params {
   int* status;
   unsigned long long* work;  // deposit: next unclaimed particle of the span
   unsigned* skip;            // one bit per span particle the mover did not store
+  const float* emax;         // max |E| over the nodes (end of the cell records)
+  float bc_eps[3];           // rounding slack of the boundary-skip test per axis
 };
 
 constexpr int kRow = 36;  // staged row stride (floats): conflict-free LDS.128 per warp
@@ -117,6 +119,18 @@ __device__ __forceinline__ void fold_commit(float& q, float& vel, float o, float
   }
 }
 
+// True when no position of the push can leave the box: the implicit
+// rotation never lengthens t = v + qdt2m E (|v_bar| <= |t|),
+// and |E| at any point is at most its node maximum, so every midpoint and the
+// committed position lie within dt * (|v|_1 + |qdt2m| max|E|) of the start.
+__device__ __forceinline__ bool interior(const Params& a, float qe, float x, float y, float z,
+                                         float u, float v, float w) {
+  const float reach = (fabsf(u) + fabsf(v) + fabsf(w) + qe) * a.dt;
+  return x - a.o[0] > reach + a.bc_eps[0] && a.hi[0] - x > reach + a.bc_eps[0] &&
+         y - a.o[1] > reach + a.bc_eps[1] && a.hi[1] - y > reach + a.bc_eps[1] &&
+         z - a.o[2] > reach + a.bc_eps[2] && a.hi[2] - z > reach + a.bc_eps[2];
+}
+
 // cell of an in-box position: truncation (in-box gx >= -ulp truncates to 0)
 // and the upper-face clamp of kernels.py:541-556; returns the cell index
 __device__ __forceinline__ int cell_of(const Params& a, float x, float y, float z, float& fx,
@@ -149,9 +163,12 @@ __device__ __forceinline__ F2 tri2(const float4& A, const float4& B, const float
   return fma2(fma2(t, FY, r), FZ, fma2(q, FY, p));
 }
 
+// skipbc (warp-uniform): the caller has shown that no position of this push
+// can leave the box (interior()), so the boundary folds and checks are
+// identities and are skipped.
 template <bool RX, bool RY, bool RZ, bool REUSE>
 __device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float& zp, float& un,
-                                    float& vn, float& wn) {
+                                    float& vn, float& wn, bool skipbc = false) {
   float vbx = un, vby = vn, vbz = wn;
   float4 R[12];
   int held = -1;  // cell whose record is in R
@@ -159,12 +176,14 @@ __device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float
   for (int it = 0; it < a.n_iters; ++it) {
     const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
     float xm = XM.x, ym = XM.y, zm = fmaf(vbz, a.dth, zp);
-    xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
-    ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
-    zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
-    if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
-        zm > a.hi[2])
-      return ST_MIDPOINT;
+    if (!skipbc) {
+      xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+      ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+      zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+      if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
+          zm > a.hi[2])
+        return ST_MIDPOINT;
+    }
     float fx, fy, fz;
     int i, j, k;
     const int cell = cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
@@ -193,12 +212,14 @@ __device__ __forceinline__ int push(const Params& a, float& xp, float& yp, float
   }
   float xo = fmaf(vbx, a.dt, xp), yo = fmaf(vby, a.dt, yp), zo = fmaf(vbz, a.dt, zp);
   float uo = 2.0f * vbx - un, vo = 2.0f * vby - vn, wo = 2.0f * vbz - wn;
-  fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
-  fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
-  fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
-  if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
-      zo > a.hi[2])
-    return ST_RUNAWAY;
+  if (!skipbc) {
+    fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+    fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+    fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+    if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
+        zo > a.hi[2])
+      return ST_RUNAWAY;
+  }
   xp = xo; yp = yo; zp = zo;
   un = uo; vn = vo; wn = wo;
   return ST_OK;
@@ -299,6 +320,8 @@ __global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ P
   };
   fetch(r, n1);
   if (PF) fetch(r + stride, n2);
+  // |qdt2m| max|E| (+1e-5 relative slack for the f32 coefficient rounding)
+  const float qe = fabsf(a.qdt2m) * __ldg(a.emax) * 1.00001f;
   const long long rbase = r - (threadIdx.x & 31);  // warp-uniform loop bound
   for (long long rb = rbase; rb < a.count; rb += stride, r += stride) {
     float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
@@ -317,9 +340,12 @@ __global__ void __launch_bounds__(256, MINB) mover_f32(const __grid_constant__ P
       fetch(r + stride, n1);
     }
     int st = ST_OK;
+    // warp-uniform: the whole warp takes the boundary-free push when it can
+    const bool all_in =
+        __all_sync(0xffffffffu, r >= a.count || interior(a, qe, xp, yp, zp, un, vn, wn));
     if (r < a.count) {
       const long long p = a.start + r;
-      st = push<RX, RY, RZ, REUSE>(a, xp, yp, zp, un, vn, wn);
+      st = push<RX, RY, RZ, REUSE>(a, xp, yp, zp, un, vn, wn, all_in);
       if (st == ST_OK) {
         __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
         __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
@@ -647,7 +673,8 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
 // (c0a c0b c1a c1b) (c2a c2b c4a c4b) (c3a c3b c5a c5b) (c6a c6b c7a c7b).
 template <typename F>
 __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int nx, int ny,
-                           int nz, float4* __restrict__ rec) {
+                           int nz, float4* __restrict__ rec, unsigned* __restrict__ emax_bits) {
+  double e2max = 0.0;  // max over nodes of |E|^2 (the mover's boundary-skip bound)
   const int NY = ny + 1, NZ = nz + 1, NN = (nx + 1) * NY * NZ;
   const int ncell = nx * ny * nz;
   // component of pair slot (pair p, member h): Ex Ey | Bx By | Ez Bz
@@ -660,12 +687,17 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
     const int n0 = (i * NY + j) * NZ + k;
     const int sx = NY * NZ, sy = NZ;
     float co[6][8];
+    double e2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int h = 0; h < 6; ++h) {
       const int m = comp[h];
       const F* f = (m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN) + n0;
       const double f000 = f[0], f100 = f[sx], f010 = f[sy], f110 = f[sx + sy];
       const double f001 = f[1], f101 = f[sx + 1], f011 = f[sy + 1], f111 = f[sx + sy + 1];
+      if (m < 3) {
+        e2[0] += f000 * f000; e2[1] += f100 * f100; e2[2] += f010 * f010; e2[3] += f110 * f110;
+        e2[4] += f001 * f001; e2[5] += f101 * f101; e2[6] += f011 * f011; e2[7] += f111 * f111;
+      }
       co[h][0] = (float)f000;
       co[h][1] = (float)(f100 - f000);
       co[h][2] = (float)(f010 - f000);
@@ -685,7 +717,14 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
       o[4 * pr + 2] = make_float4(A[3], Bq[3], A[5], Bq[5]);
       o[4 * pr + 3] = make_float4(A[6], Bq[6], A[7], Bq[7]);
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) e2max = fmax(e2max, e2[q]);
   }
+  // non-negative floats order like their bit patterns; rounded up
+  unsigned bits = __float_as_uint(__double2float_ru(sqrt(e2max)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+  if ((threadIdx.x & 31) == 0 && bits) atomicMax(emax_bits, bits);
 }
 
 }  // namespace f32k
@@ -792,7 +831,8 @@ int launch_deposit(const f32k::Params& a, cudaStream_t s) {
 
 // Number of bytes of cell records for a grid (12 float4 per cell).
 size_t f32_records_bytes(const int64_t* geo_i) {
-  return (size_t)geo_i[0] * geo_i[1] * geo_i[2] * 12 * sizeof(float4);
+  // 12 float4 per cell, then 32 bytes: max |E| over the nodes (float)
+  return (size_t)geo_i[0] * geo_i[1] * geo_i[2] * 12 * sizeof(float4) + 32;
 }
 
 int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* geo_i,
@@ -802,12 +842,14 @@ int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* ge
   int blocks = (int)((ncell + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   const int th = timing_begin(TK_RECORDS, s);
+  unsigned* emax = reinterpret_cast<unsigned*>((char*)rec + (size_t)ncell * 12 * sizeof(float4));
+  cudaMemsetAsync(emax, 0, 32, s);
   if (fbytes == 8)
     f32k::pack_cells<double><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B, nx, ny,
-                                                     nz, (float4*)rec);
+                                                     nz, (float4*)rec, emax);
   else
     f32k::pack_cells<float><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B, nx, ny, nz,
-                                                    (float4*)rec);
+                                                    (float4*)rec, emax);
   timing_end(th, s);
   note_launch();
   cudaError_t e = cudaGetLastError();
@@ -840,6 +882,7 @@ int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
     const double go = (double)(c.fbytes == 8 ? c.geo_g[3 + k] : (double)(float)c.geo_g[3 + k]);
     a.idx[k] = (float)(1.0 / gd);
     a.ogs[k] = (float)(go / gd);
+    a.bc_eps[k] = (float)(1e-5 * (fabs((double)o) + (double)L) + 1e-30);
   }
   a.dt = (float)c.dt; a.dth = (float)c.dth; a.qdt2m = (float)c.qdt2m;
   a.beta = (float)c.beta;
@@ -865,6 +908,7 @@ int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
     rc = f32_pack_records(c.fbytes, c.E, c.B, c.geo_i, rec, s);
   }
   a.rec = (const float4*)rec;
+  a.emax = reinterpret_cast<const float*>((const char*)rec + (f32_records_bytes(c.geo_i) - 32));
   static int fusedk = -1;
   if (fusedk < 0) {
     const char* env = getenv("BP_F32_FUSED");
