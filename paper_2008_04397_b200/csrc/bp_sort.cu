@@ -17,17 +17,64 @@ namespace bp {
 
 namespace {
 
+// int(t / d) exactly as the reference's f64 division then truncation
+// (geometry.py:152-159), without the division in the common case: t * (1/d)
+// is within 2 ulp of the rounded quotient, so its truncation can only differ
+// when the quotient lies within a few ulp of an integer — then divide.
+__device__ __forceinline__ int64_t cell_trunc(double t, double d, double rd) {
+  double q = t * rd;
+  if (fabs(q - rint(q)) <= 8.0 * 2.220446049250313e-16 * fmax(fabs(q), 1.0)) q = t / d;
+  return (int64_t)q;
+}
+
+// four consecutive particles per thread: 16-byte loads and stores (f32 only)
+__global__ void cell_key4_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                                 const float* __restrict__ z, int64_t n, double ox, double oy,
+                                 double oz, double dx, double dy, double dz, int64_t nx,
+                                 int64_t ny, int64_t nz, uint32_t* keys32, uint32_t* idx,
+                                 int* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double rx = 1.0 / dx, ry = 1.0 / dy, rz = 1.0 / dz;
+  const int64_t n4 = n / 4;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += stride) {
+    const float4 X = __ldcs(reinterpret_cast<const float4*>(x) + t);
+    const float4 Y = __ldcs(reinterpret_cast<const float4*>(y) + t);
+    const float4 Z = __ldcs(reinterpret_cast<const float4*>(z) + t);
+    const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w};
+    const float zs[4] = {Z.x, Z.y, Z.z, Z.w};
+    uint32_t kk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int64_t i = cell_trunc((double)xs[e] - ox, dx, rx);
+      int64_t j = cell_trunc((double)ys[e] - oy, dy, ry);
+      int64_t k = cell_trunc((double)zs[e] - oz, dz, rz);
+      i = i < nx - 1 ? i : nx - 1;
+      j = j < ny - 1 ? j : ny - 1;
+      k = k < nz - 1 ? k : nz - 1;
+      if (i < 0 || j < 0 || k < 0) {
+        *bad = 1;
+        i = j = k = 0;
+      }
+      kk[e] = (uint32_t)(i + nx * (j + ny * k));
+    }
+    __stcs(reinterpret_cast<uint4*>(keys32) + t, make_uint4(kk[0], kk[1], kk[2], kk[3]));
+    const uint32_t b = (uint32_t)(4 * t);
+    __stcs(reinterpret_cast<uint4*>(idx) + t, make_uint4(b, b + 1, b + 2, b + 3));
+  }
+}
+
 template <typename P>
 __global__ void cell_key_kernel(const P* __restrict__ x, const P* __restrict__ y,
                                 const P* __restrict__ z, int64_t n, double ox, double oy,
                                 double oz, double dx, double dy, double dz, int64_t nx,
                                 int64_t ny, int64_t nz, uint32_t* keys32, int64_t* keys64,
-                                uint32_t* idx, int* bad) {
+                                uint32_t* idx, int* bad, uint32_t idx0) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double rx = 1.0 / dx, ry = 1.0 / dy, rz = 1.0 / dz;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
-    int64_t i = (int64_t)(((double)x[p] - ox) / dx);
-    int64_t j = (int64_t)(((double)y[p] - oy) / dy);
-    int64_t k = (int64_t)(((double)z[p] - oz) / dz);
+    int64_t i = cell_trunc((double)x[p] - ox, dx, rx);
+    int64_t j = cell_trunc((double)y[p] - oy, dy, ry);
+    int64_t k = cell_trunc((double)z[p] - oz, dz, rz);
     i = i < nx - 1 ? i : nx - 1;
     j = j < ny - 1 ? j : ny - 1;
     k = k < nz - 1 ? k : nz - 1;
@@ -38,7 +85,7 @@ __global__ void cell_key_kernel(const P* __restrict__ x, const P* __restrict__ y
     const int64_t key = i + nx * (j + ny * k);
     if (keys32) keys32[p] = (uint32_t)key;
     if (keys64) keys64[p] = key;
-    if (idx) idx[p] = (uint32_t)p;
+    if (idx) idx[p] = idx0 + (uint32_t)p;
   }
 }
 
@@ -50,8 +97,18 @@ __global__ void gather_perm(const T* __restrict__ src, const uint32_t* __restric
     dst[r] = src[order[r]];
 }
 
+// 16-byte-aligned store of four consecutive elements (streaming)
+__device__ __forceinline__ void store4(float* d, float a, float b, float c, float e) {
+  __stcs(reinterpret_cast<float4*>(d), make_float4(a, b, c, e));
+}
+__device__ __forceinline__ void store4(double* d, double a, double b, double c, double e) {
+  __stcs(reinterpret_cast<double2*>(d), make_double2(a, b));
+  __stcs(reinterpret_cast<double2*>(d) + 1, make_double2(c, e));
+}
+
 // all eight particle arrays gathered through one read of the order: the
-// sorted copy lands in separate destination arrays (no copy back)
+// sorted copy lands in separate destination arrays (no copy back).  Four
+// consecutive destinations per thread: 16-byte order loads and stores.
 template <typename T>
 __global__ void gather_perm8(const T* __restrict__ x, const T* __restrict__ y,
                              const T* __restrict__ z, const T* __restrict__ u,
@@ -62,11 +119,30 @@ __global__ void gather_perm8(const T* __restrict__ x, const T* __restrict__ y,
                              T* __restrict__ ov, T* __restrict__ ow, T* __restrict__ oq,
                              long long* __restrict__ oid, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
-    const uint32_t j = __ldcs(order + r);
-    ox[r] = x[j]; oy[r] = y[j]; oz[r] = z[j];
-    ou[r] = u[j]; ov[r] = v[j]; ow[r] = w[j];
-    if (q) oq[r] = q[j];
+  const int64_t n4 = n / 4;
+  const T* src[7] = {x, y, z, u, v, w, q};
+  T* dst[7] = {ox, oy, oz, ou, ov, ow, oq};
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4; t += stride) {
+    const uint4 j = __ldcs(reinterpret_cast<const uint4*>(order) + t);
+#pragma unroll
+    for (int a = 0; a < 7; ++a) {
+      if (a == 6 && !q) break;
+      const T* sa = src[a];
+      store4(dst[a] + 4 * t, sa[j.x], sa[j.y], sa[j.z], sa[j.w]);
+    }
+    if (id) {
+      longlong2* di = reinterpret_cast<longlong2*>(oid + 4 * t);
+      __stcs(di, make_longlong2(id[j.x], id[j.y]));
+      __stcs(di + 1, make_longlong2(id[j.z], id[j.w]));
+    }
+  }
+  for (int64_t r = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const uint32_t j = order[r];
+#pragma unroll
+    for (int a = 0; a < 7; ++a) {
+      if (a == 6 && !q) break;
+      dst[a][r] = src[a][j];
+    }
     if (id) oid[r] = id[j];
   }
 }
@@ -118,19 +194,19 @@ int check(cudaError_t e, const char* what) {
 template <typename P>
 int keys_launch(const void* xs, const void* ys, const void* zs, int64_t n, const double* o,
                 const double* d, const int64_t* c, uint32_t* k32, int64_t* k64, uint32_t* idx,
-                int* bad, cudaStream_t s) {
+                int* bad, cudaStream_t s, uint32_t idx0) {
   cell_key_kernel<P><<<blocks_for(n), 256, 0, s>>>((const P*)xs, (const P*)ys, (const P*)zs, n,
                                                    o[0], o[1], o[2], d[0], d[1], d[2], c[0],
-                                                   c[1], c[2], k32, k64, idx, bad);
+                                                   c[1], c[2], k32, k64, idx, bad, idx0);
   note_launch();
   return check(cudaGetLastError(), "cell_key_kernel");
 }
 
 int keys_any(int pbytes, const void* xs, const void* ys, const void* zs, int64_t n,
              const double* o, const double* d, const int64_t* c, uint32_t* k32, int64_t* k64,
-             uint32_t* idx, int* bad, cudaStream_t s) {
-  if (pbytes == 8) return keys_launch<double>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s);
-  if (pbytes == 4) return keys_launch<float>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s);
+             uint32_t* idx, int* bad, cudaStream_t s, uint32_t idx0 = 0) {
+  if (pbytes == 8) return keys_launch<double>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s, idx0);
+  if (pbytes == 4) return keys_launch<float>(xs, ys, zs, n, o, d, c, k32, k64, idx, bad, s, idx0);
   set_error("unsupported particle dtype (%d bytes)", pbytes);
   return -1;
 }
@@ -279,8 +355,22 @@ int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* cons
   p += up((size_t)n * 8);
   void* cub_tmp = p;
   cudaMemsetAsync(bad, 0, sizeof(int), s);
-  int rc = keys_any(pbytes, src[0], src[1], src[2], n, origin, spacing, counts, k_in, nullptr,
-                    i_in, bad, s);
+  int rc = 0;
+  const int64_t n4 = pbytes == 4 ? n / 4 * 4 : 0;
+  if (n4) {
+    cell_key4_kernel<<<blocks_for(n4 / 4), 256, 0, s>>>(
+        (const float*)src[0], (const float*)src[1], (const float*)src[2], n4, origin[0],
+        origin[1], origin[2], spacing[0], spacing[1], spacing[2], counts[0], counts[1],
+        counts[2], k_in, i_in, bad);
+    note_launch();
+    rc = check(cudaGetLastError(), "cell_key4_kernel");
+  }
+  if (!rc && n4 < n) {
+    // the tail (and f64 particles): one particle per thread, indices offset
+    rc = keys_any(pbytes, (const char*)src[0] + n4 * pbytes, (const char*)src[1] + n4 * pbytes,
+                  (const char*)src[2] + n4 * pbytes, n - n4, origin, spacing, counts,
+                  k_in + n4, nullptr, i_in + n4, bad, s, (uint32_t)n4);
+  }
   if (!rc)
     rc = check(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k_in, k_out, i_in, i_out, n,
                                                0, end_bit, s),

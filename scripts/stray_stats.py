@@ -13,7 +13,7 @@ for sid, p in enumerate(init_gem_device(geom, sp, dev, precision=prec)):
     sim.load_species(sid, p)
 f = gem_fields(geom, GemInit(), prec); sim.set_fields(f.E, f.B)
 def stats(step):
-    for sid in (0, 1):
+    for sid in (0, 1, 2, 3):
         p = sim.particles[sid]
         i = ((p.x.double() / geom.dx).long().clamp(max=geom.nx - 1))
         j = ((p.y.double() / geom.dy).long().clamp(max=geom.ny - 1))
@@ -32,7 +32,7 @@ def stats(step):
         print(f"step {step} species {sid}: non-majority/tile {nonmaj.mean():.2f}, "
               f"distinct cells/tile {distinct.mean():.2f}, distinct cells/4 tiles {d4.mean():.2f}, "
               f"uniform tiles {(nonmaj == 0).double().mean():.3f}", flush=True)
-stats(0)
+sim.sort(); stats(0)
 for s in range(1, 11):
     sim.run_cycle()
     if s in (1, 2, 5, 10):
