@@ -519,47 +519,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_f32(const __grid_constant__
           pv1[k2] += T1.x + T1.y;
           if (third) pv2[k2] += T2.x + T2.y;
         }
-        if (STRAY_GROUP == 2) {
-          // two cells per round: independent fold / update chains
-          while (rest) {
-            const int ka = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
-            const unsigned MA2 = __ballot_sync(0xffffffffu, fit && pnode == ka);
-            rest &= ~MA2;
-            const int kb2 = __shfl_sync(0xffffffffu, pnode, __ffs(rest | 0x80000000u) - 1);
-            const unsigned MB2 = rest ? __ballot_sync(0xffffffffu, fit && pnode == kb2) : 0u;
-            rest &= ~MB2;
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
-            unsigned ma = MA2, mb = MB2;
-            while (ma | mb) {
-              if (ma) {
-                const int kk = __ffs(ma) - 1;
-                ma &= ma - 1u;
-                const float b = st_bs[lc * kRow + kk];
-                a0 = fmaf(b, st_mv[lg * kRow + kk], a0);
-                a1 = fmaf(b, st_mv[(lg + 4) * kRow + kk], a1);
-                a2 = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], a2);
-              }
-              if (mb) {
-                const int kk = __ffs(mb) - 1;
-                mb &= mb - 1u;
-                const float b = st_bs[lc * kRow + kk];
-                b0 = fmaf(b, st_mv[lg * kRow + kk], b0);
-                b1 = fmaf(b, st_mv[(lg + 4) * kRow + kk], b1);
-                b2 = fmaf(b, st_mv[(third ? lg + 8 : 8) * kRow + kk], b2);
-              }
-            }
-            const float pa0 = pv0[ka], pa1 = pv1[ka];
-            if (MB2) {
-              const float pb0 = pv0[kb2], pb1 = pv1[kb2];
-              pv0[kb2] = pb0 + b0;
-              pv1[kb2] = pb1 + b1;
-              if (third) pv2[kb2] += b2;
-            }
-            pv0[ka] = pa0 + a0;
-            pv1[ka] = pa1 + a1;
-            if (third) pv2[ka] += a2;
-          }
-        } else if (STRAY_GROUP) {
+        if (STRAY_GROUP) {
           const float* brow = st_bs + lc * kRow;
           const float* m0row = st_mv + lg * kRow;
           const float* m1row = st_mv + (lg + 4) * kRow;
@@ -820,7 +780,6 @@ int launch_deposit(const f32k::Params& a, cudaStream_t s) {
     case 1: return launch_deposit_cfg<8, 512, 3, true, 1>(a, s);
     case 2: return launch_deposit_cfg<8, 512, 3, false, 0>(a, s);
     case 3: return launch_deposit_cfg<12, 1024, 2, false, 1>(a, s);
-    case 4: return launch_deposit_cfg<8, 512, 3, false, 2>(a, s);
     case 5: return launch_deposit_cfg<8, 1024, 3, false, 1>(a, s);
     case 6: return launch_deposit_cfg<8, 256, 3, false, 1>(a, s);
     default: return launch_deposit_cfg<8, 512, 3, false, 1>(a, s);
@@ -892,7 +851,8 @@ int f32_fused(const Call& c, const void* rec_in, cudaStream_t s) {
   a.status = c.status;
   void* rec = const_cast<void*>(rec_in);
   const size_t rbytes = f32_records_bytes(c.geo_i);
-  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 255) & ~(size_t)255;
+  // one bit per particle, +2 words so a round's second tile may read past the end
+  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 8 + 255) & ~(size_t)255;
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, 256 + skip_bytes + (rec ? 0 : rbytes), s);
   if (e != cudaSuccess) {
