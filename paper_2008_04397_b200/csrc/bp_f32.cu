@@ -710,11 +710,21 @@ int sm_count_f32() {
   return sms;
 }
 
+// blocks per SM cap (BP_F32_MOVER_BPS / BP_F32_DEPOSIT_BPS; 0 = occupancy):
+// lets a mover and a deposit of different spans share the SMs when the
+// caller runs them on two streams
+int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
 template <bool RX, bool RY, bool RZ, bool REUSE, int MINB, bool PF = false>
 int launch_mover_cfg(const f32k::Params& a, cudaStream_t s) {
   auto k = f32k::mover_f32<RX, RY, RZ, REUSE, MINB, PF>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+  static const int cap = env_int("BP_F32_MOVER_BPS");
+  if (cap > 0 && per_sm > cap) per_sm = cap;
   if (per_sm < 1) per_sm = 1;
   const long long need = (a.count + 255) / 256;
   long long g = (long long)sm_count_f32() * per_sm;
@@ -755,6 +765,8 @@ int launch_deposit_cfg(const f32k::Params& a, cudaStream_t s) {
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  static const int cap = env_int("BP_F32_DEPOSIT_BPS");
+  if (cap > 0 && per_sm > cap) per_sm = cap;
   if (per_sm < 1) per_sm = 1;
   const long long need = (a.count + CHUNK * 8 - 1) / (CHUNK * 8);
   long long g = (long long)sm_count_f32() * per_sm;

@@ -198,6 +198,21 @@ class DeviceSimulation:
             ptr(self.status), ctypes.c_void_p(stream.cuda_stream))
         _lib.check(rc, "fused_span")
 
+    def _side_streams(self, s):
+        """Species on alternating side streams (env BP_SPECIES_STREAMS=2):
+        one species' deposit may then share the SMs with the next one's
+        mover.  The side streams start after everything queued on `s`."""
+        import os
+        n = int(os.environ.get("BP_SPECIES_STREAMS", "0"))
+        if n <= 1:
+            return []
+        torch = self.torch
+        if getattr(self, "_side", None) is None or len(self._side) != n:
+            self._side = [torch.cuda.Stream(device=self.device) for _ in range(n)]
+        for ss in self._side:
+            ss.wait_stream(s)
+        return self._side
+
     def phase3(self, reduce=True):
         """Phases 2-3 for every species; returns (phase3_ms, kernel_ms) of
         device time on the compute stream (events), reduce included."""
@@ -210,14 +225,20 @@ class DeviceSimulation:
             a.zero_()
         ev[1].record(s)
         works = []
+        side = self._side_streams(s)
         for sid, p in enumerate(self.particles):
             if p is None or p.n == 0:
                 continue
+            ss = side[sid % len(side)] if side else s
             for (b0, bn) in partition_batches(p.n, self.batches).spans:
                 if bn:
-                    self._fused(sid, b0, bn, s)
+                    self._fused(sid, b0, bn, ss)
             if reduce and self.distributed:
+                if side:
+                    s.wait_stream(ss)
                 works += reduce_moments([self.acc[sid]], self.group, async_op=True)
+        for ss in side:
+            s.wait_stream(ss)
         ev[2].record(s)
         for w in works:
             w.wait()

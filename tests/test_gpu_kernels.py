@@ -336,3 +336,57 @@ def test_fast_f32_every_boundary_kind(gpu, oracle, bc, failing):
     got = dacc.cpu().numpy()
     for m in range(10):
         _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, 1e-4)
+
+
+def test_prepared_records_and_timing_api(gpu):
+    """bp_field_records_build + bp_fused_span_rec give the same bits as the
+    per-call record build, and bp_timing_read reports the f32 kernels."""
+    import ctypes
+    from paper_2008_04397_b200 import _lib
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    L = _lib.load()
+    n = 100_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state("single", n, seed=7,
+                                                                       order="sorted")
+    inv = geom.inv_node_volume(fd)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+            fd(SCALE), 0)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    d1 = _dev(torch, arrs)
+    acc1 = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    L.bp_timing_enable(1)
+    _lib.timing_read()
+    st1 = K.fused_span(*d1, 0, n, dE, dB, acc1, dinv, *tail, arith="fast")
+    t = _lib.timing_read()
+    L.bp_timing_enable(0)
+    assert t["mover"][1] == 1 and t["deposit"][1] == 1 and t["records"][1] == 1
+    assert t["mover"][0] > 0.0 and t["deposit"][0] > 0.0
+    gi = np.ascontiguousarray(geo_i, np.int64)
+    nbytes = L.bp_field_records_bytes(ctypes.c_void_p(gi.ctypes.data))
+    assert nbytes > 0
+    rec = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
+    ptr = (rec.data_ptr() + 255) & ~255
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.bp_field_records_build(4, ctypes.c_void_p(dE.data_ptr()),
+                                    ctypes.c_void_p(dB.data_ptr()),
+                                    ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
+                                    stream) == 0
+    # misaligned records are refused
+    assert L.bp_field_records_build(4, ctypes.c_void_p(dE.data_ptr()),
+                                    ctypes.c_void_p(dB.data_ptr()),
+                                    ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr + 4),
+                                    stream) == _lib.EINVAL
+    d2 = _dev(torch, arrs)
+    acc2 = torch.zeros_like(acc1)
+    hp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    gf, gg = (np.ascontiguousarray(g, np.float64) for g in (geo_f, geo_g))
+    st2 = L.bp_fused_span_rec(_lib.ARITH_FAST, 4, 4, *[ctypes.c_void_p(a.data_ptr()) for a in d2],
+                              0, n, ctypes.c_void_p(dE.data_ptr()), ctypes.c_void_p(dB.data_ptr()),
+                              ctypes.c_void_p(acc2.data_ptr()), ctypes.c_void_p(dinv.data_ptr()),
+                              hp(gf), hp(gg), hp(gi), float(sc["dt"]), float(sc["dth"]),
+                              float(sc["qdt2m"]), float(sc["beta"]), float(sc["one"]), 3,
+                              float(SCALE), 0, ctypes.c_void_p(ptr), None, stream)
+    assert st2 == st1
+    assert torch.equal(acc1, acc2)
+    assert all(torch.equal(a, b) for a, b in zip(d1, d2))
