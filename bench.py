@@ -48,7 +48,7 @@ METRIC = ("particles moved+interpolated/sec (GEM 3D) at 1/2/4/8 B200; HBM GB/s f
 UNIT = "particles/s"
 BYTES_PER_PARTICLE = {"single": 52, "mixed": 52, "double": 104}  # 13 words, SURVEY §8d
 # algorithmic words per particle of each kernel of the f32 fast path
-# (bp_f32.cu): the mover reads and writes x y z u v w, the deposit reads
+# (bp_split.cu): the mover reads and writes x y z u v w, the deposit reads
 # x y z u v w q
 KERNEL_WORDS = {"mover": 12, "deposit": 7, "span": 13}
 
@@ -322,8 +322,8 @@ def main_ours(args):
                         "share_of_step": ms / elapsed_ms}
     dom = max(kinfo, key=lambda k: kinfo[k]["ms_per_launch"] * kinfo[k]["launches"])
     dk = kinfo[dom]
-    names = {"mover": "bp::f32k::mover_f32 (implicit mover, 3 iterations)",
-             "deposit": "bp::f32k::deposit_f32 (10-moment interpolation)",
+    names = {"mover": "bp::sk::mover_kernel (implicit mover, 3 iterations)",
+             "deposit": "bp::sk::deposit_kernel (10-moment interpolation)",
              "span": "bp::span_kernel (generic fused mover + deposit)"}
     traffic = ncu_traffic(dom) if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
                                    and args.precision == "single"

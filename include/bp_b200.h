@@ -123,18 +123,18 @@ int bp_fused_span_ex(int arith, int pbytes, int fbytes, void* xs, void* ys, void
                      double dth, double qdt2m, double beta, double one, int n_iters,
                      double scale, int mixed, int* d_status, void* stream);
 
-/* Per-cell field records for the f32 fast kernels (bp_f32.cu): for every
- * cell the trilinear coefficients of Ex Ey Ez Bx By Bz (48 floats).  The
- * fused call builds them from E / B on its stream unless the caller passes
- * records built once per field update: bp_field_records_bytes() gives the
- * size of the (32-byte aligned) device buffer, bp_field_records_build()
- * fills it from E, B (fbytes 4 or 8), and bp_fused_span_rec() is
- * bp_fused_span_ex() with a `records` argument (NULL = build per call;
- * ignored by the parity and f64 kernels).  The records must describe the E,
- * B passed to the call. */
-int64_t bp_field_records_bytes(const int64_t* geo_i);
-int bp_field_records_build(int fbytes, const void* E, const void* B, const int64_t* geo_i,
-                           void* records, void* stream);
+/* Per-cell field records of the fast kernels (csrc/bp_split.cu): for every
+ * cell the trilinear coefficients of Ex Ey Ez Bx By Bz (48 values in the
+ * particle precision).  The fused call builds them from E / B on its stream
+ * unless the caller passes records built once per field update:
+ * bp_field_records_bytes() gives the size of the (32-byte aligned) device
+ * buffer for particles of pbytes, bp_field_records_build() fills it from E,
+ * B, and bp_fused_span_rec() is bp_fused_span_ex() with a `records` argument
+ * (NULL = build per call; ignored by the parity kernels).  The records must
+ * describe the E, B passed to the call. */
+int64_t bp_field_records_bytes(int pbytes, const int64_t* geo_i);
+int bp_field_records_build(int pbytes, int fbytes, const void* E, const void* B,
+                           const int64_t* geo_i, void* records, void* stream);
 int bp_fused_span_rec(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
                       void* vs, void* ws, const void* qs, int64_t start, int64_t count,
                       const void* E, const void* B, int64_t* acc, const void* invvol,

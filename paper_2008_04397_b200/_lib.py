@@ -49,10 +49,10 @@ _SIGS = {
     "bp_fused_span_rec": (_INT, [_INT, _INT, _INT] + [_P] * 7 + [_I64, _I64]
                           + [_P] * 4 + [_P, _P, _P] + [_D] * 5
                           + [_INT, _D, _INT, _P, _P, _P]),
-    "bp_field_records_bytes": (_I64, [_P]),
+    "bp_field_records_bytes": (_I64, [_INT, _P]),
     "bp_timing_enable": (_INT, [_INT]),
     "bp_timing_read": (_INT, [_P, _P, _INT]),
-    "bp_field_records_build": (_INT, [_INT, _P, _P, _P, _P, _P]),
+    "bp_field_records_build": (_INT, [_INT, _INT, _P, _P, _P, _P, _P]),
     "bp_push_span": (_INT, [_INT, _INT] + [_P] * 6 + [_I64, _I64, _P, _P]
                      + [_P, _P, _P] + [_D] * 5 + [_INT, _INT, _INT, _P, _P]),
     "bp_deposit_span": (_INT, [_INT, _INT] + [_P] * 7 + [_I64, _I64, _P, _P,

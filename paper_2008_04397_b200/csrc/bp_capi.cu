@@ -359,18 +359,22 @@ int bp_fused_span_ex(int arith, int pbytes, int fbytes, void* xs, void* ys, void
                     mixed, d_status, (cudaStream_t)stream);
 }
 
-int64_t bp_field_records_bytes(const int64_t* geo_i) {
+int64_t bp_field_records_bytes(int pbytes, const int64_t* geo_i) {
+  if (pbytes != 4 && pbytes != 8) {
+    set_error("particle dtype must be 4 or 8 bytes");
+    return BP_EINVAL;
+  }
   if (!geo_i || geo_i[0] < 1 || geo_i[1] < 1 || geo_i[2] < 1) {
     set_error("cell counts must be >= 1");
     return BP_EINVAL;
   }
-  return (int64_t)f32_records_bytes(geo_i);
+  return (int64_t)split_records_bytes(pbytes, geo_i);
 }
 
-int bp_field_records_build(int fbytes, const void* E, const void* B, const int64_t* geo_i,
-                           void* records, void* stream) {
-  if (fbytes != 4 && fbytes != 8) {
-    set_error("field dtype must be 4 or 8 bytes");
+int bp_field_records_build(int pbytes, int fbytes, const void* E, const void* B,
+                           const int64_t* geo_i, void* records, void* stream) {
+  if (!valid_pair(pbytes, fbytes)) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
     return BP_EINVAL;
   }
   if (!E || !B || !records || !geo_i) {
@@ -385,7 +389,9 @@ int bp_field_records_build(int fbytes, const void* E, const void* B, const int64
     set_error("records must be 32-byte aligned");
     return BP_EINVAL;
   }
-  return f32_pack_records(fbytes, E, B, geo_i, records, (cudaStream_t)stream) ? BP_ECUDA : BP_OK;
+  return split_pack_records(pbytes, fbytes, E, B, geo_i, records, (cudaStream_t)stream)
+             ? BP_ECUDA
+             : BP_OK;
 }
 
 int bp_fused_span_rec(int arith, int pbytes, int fbytes, void* xs, void* ys, void* zs, void* us,
@@ -511,7 +517,7 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
   // f32 fast path: the cell records of E/B once for all batches
   const bool f32rec = arith == BP_ARITH_FAST && pbytes == 4;
   if (f32rec && !rc) {
-    const size_t rb = f32_records_bytes(geo_i) + 256;
+    const size_t rb = split_records_bytes(pbytes, geo_i) + 256;
     if (rb > h.rec_bytes) {
       if (h.rec) cudaFree(h.rec);
       h.rec = nullptr;
@@ -519,7 +525,7 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
       rc = cuda_check(cudaMalloc(&h.rec, rb), "records alloc");
       if (!rc) h.rec_bytes = rb;
     }
-    if (!rc) rc = f32_pack_records(fbytes, h.dE, h.dB, geo_i, h.rec, s0) ? BP_ECUDA : BP_OK;
+    if (!rc) rc = split_pack_records(pbytes, fbytes, h.dE, h.dB, geo_i, h.rec, s0) ? BP_ECUDA : BP_OK;
   }
   rc |= cuda_check(cudaEventRecord(h.ready[0], s0), "event");
   if (rc) return rc < 0 ? rc : BP_ECUDA;

@@ -25,7 +25,7 @@ struct Call {
   int n_iters, mixed, apply_bc;
   void* out;    // gather rows
   int* status;  // device int, atomicMax
-  const void* records;  // prebuilt f32 cell records (bp_field_records_build) or NULL
+  const void* records;  // prebuilt cell records (bp_field_records_build) or NULL
 };
 
 // Return 0 on a successful enqueue, else a negative BP_E* code.
@@ -34,13 +34,14 @@ int launch_fast(const Call& c, cudaStream_t s);
 
 void set_error(const char* fmt, ...);
 
-// f32 particles, fast arithmetic, fused op (bp_f32.cu): per-cell coefficient
-// records `rec` (f32_records_bytes) prebuilt by f32_pack_records, or NULL to
-// build them on the stream for this call.
-size_t f32_records_bytes(const int64_t* geo_i);
-int f32_pack_records(int fbytes, const void* E, const void* B, const int64_t* geo_i, void* rec,
-                     cudaStream_t s);
-int f32_fused(const Call& c, const void* rec, cudaStream_t s);
+// Fast arithmetic, fused op, as the mover + deposit kernel pair of
+// bp_split.cu (f32 particles with f32 or f64 fields, and f64 / f64): per-cell
+// coefficient records `rec` (split_records_bytes, particle precision) built
+// by split_pack_records, or NULL to build them on the stream for this call.
+size_t split_records_bytes(int pbytes, const int64_t* geo_i);
+int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
+                       const int64_t* geo_i, void* rec, cudaStream_t s);
+int split_fused(const Call& c, const void* rec, cudaStream_t s);
 
 // count of kernels this library launched (bp_kernel_launches)
 void note_launch(int n = 1);

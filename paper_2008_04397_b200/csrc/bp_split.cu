@@ -1,0 +1,886 @@
+// The fast-arithmetic fused span as two kernels — the implicit mover and the
+// 10-moment interpolation (deposit) — for f32 particles ("single" / "mixed"),
+// sm_100a.  The code is written for T = float or double; the f64
+// instantiation is not dispatched (see split_fused).  Same algorithm as the
+// reference fused_span (pkg/src/batchpic/kernels.py:458-735); DESIGN.md §4
+// has the instruction budget and the measurements behind every choice here.
+//
+// Cell records (pack_cells): for each cell, in the particles' sort order
+// (x fastest), the trilinear form of the 6 components
+//     f(fx,fy,fz) = [c0 + c1 fx + (c2 + c4 fx) fy] + fz [c3 + c5 fx + (c6 + c7 fx) fy]
+// (the reference's 8-weight sum, kernels.py:557-591, regrouped), components
+// paired (Ex Ey | Bx By | Ez Bz): 12 quads of T per cell.  For f32 the pairs
+// are evaluated with the packed FP32 instruction FFMA2 (two f32 lanes per
+// instruction, sm_100): 21 FFMA2 per gather.  The f32 mover keeps the record
+// in registers while the midpoint stays in its cell.
+//
+// Mover: one particle per thread, persistent grid, next particle prefetched,
+// boundary kinds as template parameters, boundary folds skipped for warps
+// that provably stay inside (interior()).  Failed particles (runaway,
+// midpoint) are not stored and get a bit in the `skip` bitmask.
+//
+// Deposit: per-warp transposed fold (lane = corner x moment group, tiles of
+// 32 staged particles) into a per-warp node patch in shared memory, flushed
+// onto the int64 lattice (x invvol x 2^43, rint) with REDG.ADD.64.  A tile's
+// partial sums are formed in T and rounded once onto the lattice — within
+// the north star's 1e-4 for f32 — and every chunk is flushed on its own, so
+// the result is deterministic for a given launch.
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "bp_common.cuh"
+#include "bp_launch.h"
+
+namespace bp {
+namespace sk {
+
+template <typename T>
+struct Params {
+  T *x, *y, *z, *u, *v, *w;
+  const T* q;
+  long long start, count;
+  const void* rec;     // 12 quads of T per cell, cell = i + nx * (j + ny * k)
+  const float* iv_f;   // invvol (nx+1, ny+1, nz+1) when fields are f32
+  const double* iv_d;  // ... when fields are f64
+  long long* acc;      // (10, NN) int64
+  int nx, ny, nz, NY, NZ, NN;
+  int cny;  // nx * ny (cell-record z stride)
+  T o[3], hi[3], L[3], hi2[3], idx[3], ogs[3];
+  T dt, dth, qdt2m, beta, beta2;
+  double scale;
+  int n_iters;
+  int* status;
+  unsigned long long* work;  // deposit: next unclaimed particle of the span
+  unsigned* skip;            // one bit per span particle the mover did not store
+  const float* emax;         // max |E| over the nodes (after the cell records)
+  T bc_eps[3];               // rounding slack of the boundary-skip test per axis
+};
+
+// record quad of T
+template <typename T>
+struct Quad;
+template <>
+struct Quad<float> {
+  typedef float4 type;
+};
+template <>
+struct Quad<double> {
+  typedef double4 type;
+};
+
+// staged row stride (elements): rows read by one warp LDS.128 land in
+// distinct banks (36 floats / 34 doubles = 4 mod 32 words)
+template <typename T>
+__host__ __device__ constexpr int row_len() {
+  return sizeof(T) == 4 ? 36 : 34;
+}
+// staging rows: 8 bases (corner c), then 10 moments (row 8 + m; m = 0 is 1)
+template <typename T>
+__host__ __device__ constexpr int stage_len() {
+  return 18 * row_len<T>();
+}
+
+__device__ __forceinline__ float rcp_fast(float d) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));  // d >= 1: MUFU.RCP alone
+  return r;
+}
+__device__ __forceinline__ double rcp_fast(double d) { return __drcp_rn(d); }
+
+// record loads (kept in L1 / L2 in preference to the particle streams)
+__device__ __forceinline__ void ldg_pair(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.L1::evict_last.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void ldg_pair(const double4* p, double4& a, double4& b) {
+  asm("ld.global.nc.L1::evict_last.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(a.z), "=d"(a.w)
+      : "l"(p));
+  asm("ld.global.nc.L1::evict_last.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(b.x), "=d"(b.y), "=d"(b.z), "=d"(b.w)
+      : "l"(p + 1));
+}
+
+template <bool REFL, typename T>
+__device__ __forceinline__ T fold_mid(T xm, T o, T L, T hi, T hi2) {
+  if (!REFL) {
+    if (xm < o) xm += L;
+    else if (xm > hi) xm -= L;
+  } else {
+    if (xm < o) xm = o + (o - xm);
+    else if (xm > hi) xm = hi2 - xm;
+  }
+  return xm;
+}
+
+template <bool REFL, typename T>
+__device__ __forceinline__ void fold_commit(T& q, T& vel, T o, T L, T hi, T hi2) {
+  if (!REFL) {
+    if (q < o) {
+      q += L;
+      if (q >= hi) q = o;
+    } else if (q >= hi) {
+      q -= L;
+    }
+  } else {
+    if (q < o) {
+      q = o + (o - q);
+      vel = -vel;
+    } else if (q > hi) {
+      q = hi2 - q;
+      vel = -vel;
+    }
+  }
+}
+
+// True when no position of the push can leave the box: the implicit
+// rotation never lengthens t = v + qdt2m E (|v_bar| <= |t|),
+// and |E| at any point is at most its node maximum, so every midpoint and the
+// committed position lie within dt * (|v|_1 + |qdt2m| max|E|) of the start.
+template <typename T>
+__device__ __forceinline__ bool interior(const Params<T>& a, T qe, T x, T y, T z, T u, T v,
+                                         T w) {
+  const T reach = (fabs(u) + fabs(v) + fabs(w) + qe) * a.dt;
+  return x - a.o[0] > reach + a.bc_eps[0] && a.hi[0] - x > reach + a.bc_eps[0] &&
+         y - a.o[1] > reach + a.bc_eps[1] && a.hi[1] - y > reach + a.bc_eps[1] &&
+         z - a.o[2] > reach + a.bc_eps[2] && a.hi[2] - z > reach + a.bc_eps[2];
+}
+
+// cell of an in-box position: truncation (in-box gx >= -ulp truncates to 0)
+// and the upper-face clamp of kernels.py:541-556; returns the cell index
+template <typename T>
+__device__ __forceinline__ int cell_of(const Params<T>& a, T x, T y, T z, T& fx, T& fy, T& fz,
+                                       int& i, int& j, int& k) {
+  const T gx = fma(x, a.idx[0], -a.ogs[0]);
+  const T gy = fma(y, a.idx[1], -a.ogs[1]);
+  const T gz = fma(z, a.idx[2], -a.ogs[2]);
+  i = min((int)gx, a.nx - 1);
+  j = min((int)gy, a.ny - 1);
+  k = min((int)gz, a.nz - 1);
+  fx = gx - (T)i;
+  fy = gy - (T)j;
+  fz = gz - (T)k;
+  return i + a.nx * j + a.cny * k;
+}
+
+typedef float2 F2;
+__device__ __forceinline__ F2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
+
+// one component pair (a, b) from its four quads: A = c0a c0b c1a c1b,
+// B = c2a c2b c4a c4b, C = c3a c3b c5a c5b, D = c6a c6b c7a c7b
+__device__ __forceinline__ void tri_pair(const float4& A, const float4& B, const float4& C,
+                                         const float4& D, float fx, float fy, float fz,
+                                         float& ra, float& rb) {
+  const F2 FX = f2(fx, fx), FY = f2(fy, fy), FZ = f2(fz, fz);
+  const F2 p = fma2(f2(A.z, A.w), FX, f2(A.x, A.y));
+  const F2 q = fma2(f2(B.z, B.w), FX, f2(B.x, B.y));
+  const F2 r = fma2(f2(C.z, C.w), FX, f2(C.x, C.y));
+  const F2 t = fma2(f2(D.z, D.w), FX, f2(D.x, D.y));
+  const F2 o = fma2(fma2(t, FY, r), FZ, fma2(q, FY, p));
+  ra = o.x;
+  rb = o.y;
+}
+__device__ __forceinline__ void tri_pair(const double4& A, const double4& B, const double4& C,
+                                         const double4& D, double fx, double fy, double fz,
+                                         double& ra, double& rb) {
+  ra = fma(fma(fma(D.z, fx, D.x), fy, fma(C.z, fx, C.x)), fz,
+           fma(fma(B.z, fx, B.x), fy, fma(A.z, fx, A.x)));
+  rb = fma(fma(fma(D.w, fx, D.y), fy, fma(C.w, fx, C.y)), fz,
+           fma(fma(B.w, fx, B.y), fy, fma(A.w, fx, A.y)));
+}
+
+// skipbc (warp-uniform): the caller has shown that no position of this push
+// can leave the box (interior()), so the boundary folds and checks are
+// identities and are skipped.
+template <typename T, bool RX, bool RY, bool RZ, bool REUSE>
+__device__ __forceinline__ int push(const Params<T>& a, T& xp, T& yp, T& zp, T& un, T& vn,
+                                    T& wn, bool skipbc) {
+  typedef typename Quad<T>::type Q;
+  T vbx = un, vby = vn, vbz = wn;
+  Q R[12];
+  int held = -1;  // cell whose record is in R
+#pragma unroll 1
+  for (int it = 0; it < a.n_iters; ++it) {
+    T xm, ym;
+    if constexpr (std::is_same<T, float>::value) {
+      const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
+      xm = XM.x;
+      ym = XM.y;
+    } else {
+      xm = fma(vbx, a.dth, xp);
+      ym = fma(vby, a.dth, yp);
+    }
+    T zm = fma(vbz, a.dth, zp);
+    if (!skipbc) {
+      xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+      ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+      zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+      if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
+          zm > a.hi[2])
+        return ST_MIDPOINT;
+    }
+    T fx, fy, fz;
+    int i, j, k;
+    const int cell = cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    if (!REUSE || cell != held) {
+      held = cell;
+      const Q* r = static_cast<const Q*>(a.rec) + (size_t)cell * 12;
+#pragma unroll
+      for (int q = 0; q < 12; q += 2) ldg_pair(r + q, R[q], R[q + 1]);
+    }
+    T ex, ey, hx, hy, ez, hz;
+    tri_pair(R[0], R[1], R[2], R[3], fx, fy, fz, ex, ey);
+    tri_pair(R[4], R[5], R[6], R[7], fx, fy, fz, hx, hy);
+    tri_pair(R[8], R[9], R[10], R[11], fx, fy, fz, ez, hz);
+    T tx, ty;
+    if constexpr (std::is_same<T, float>::value) {
+      const F2 Txy = fma2(f2(a.qdt2m, a.qdt2m), f2(ex, ey), f2(un, vn));
+      tx = Txy.x;
+      ty = Txy.y;
+    } else {
+      tx = fma(a.qdt2m, ex, un);
+      ty = fma(a.qdt2m, ey, vn);
+    }
+    const T tz = fma(a.qdt2m, ez, wn);
+    const T bsq = fma(hx, hx, fma(hy, hy, hz * hz));
+    const T inv = rcp_fast(fma(a.beta2, bsq, T(1)));
+    const T tdb = fma(tx, hx, fma(ty, hy, tz * hz));
+    const T bt = a.beta * tdb;
+    const T cx = fma(ty, hz, -tz * hy), cy = fma(tz, hx, -tx * hz), cz = fma(tx, hy, -ty * hx);
+    vbx = fma(a.beta, fma(bt, hx, cx), tx) * inv;
+    vby = fma(a.beta, fma(bt, hy, cy), ty) * inv;
+    vbz = fma(a.beta, fma(bt, hz, cz), tz) * inv;
+  }
+  T xo = fma(vbx, a.dt, xp), yo = fma(vby, a.dt, yp), zo = fma(vbz, a.dt, zp);
+  T uo = T(2) * vbx - un, vo = T(2) * vby - vn, wo = T(2) * vbz - wn;
+  if (!skipbc) {
+    fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+    fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+    fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+    if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
+        zo > a.hi[2])
+      return ST_RUNAWAY;
+  }
+  xp = xo; yp = yo; zp = zo;
+  un = uo; vn = vo; wn = wo;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Mover: one particle per thread, coalesced SoA streams, no shared memory, so
+// the SM holds enough warps to hide the latency of the dependent gather +
+// rotation steps.  Particles that fail (kernels.py:618-621, 672-676) are not
+// stored; their bit in `skip` keeps them out of the deposit.
+template <typename T, bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+__global__ void __launch_bounds__(256, MINB) mover_kernel(const __grid_constant__ Params<T> a) {
+  // persistent grid: each thread walks particles r, r + stride, ... with the
+  // next particle's loads in flight while the current one is pushed
+  const long long stride = (long long)gridDim.x * 256;
+  long long r = (long long)blockIdx.x * 256 + threadIdx.x;
+  T n1[6] = {0, 0, 0, 0, 0, 0};
+  auto fetch = [&](long long rr) {
+    if (rr < a.count) {
+      const long long p = a.start + rr;
+      n1[0] = __ldcs(a.x + p); n1[1] = __ldcs(a.y + p); n1[2] = __ldcs(a.z + p);
+      n1[3] = __ldcs(a.u + p); n1[4] = __ldcs(a.v + p); n1[5] = __ldcs(a.w + p);
+    }
+  };
+  fetch(r);
+  // |qdt2m| max|E| (+1e-5 relative slack for the coefficient rounding)
+  const T qe = fabs(a.qdt2m) * (T)__ldg(a.emax) * T(1.00001);
+  const long long rbase = r - (threadIdx.x & 31);  // warp-uniform loop bound
+  for (long long rb = rbase; rb < a.count; rb += stride, r += stride) {
+    T xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
+    fetch(r + stride);
+    int st = ST_OK;
+    // warp-uniform: the whole warp takes the boundary-free push when it can
+    const bool all_in =
+        __all_sync(0xffffffffu, r >= a.count || interior(a, qe, xp, yp, zp, un, vn, wn));
+    if (r < a.count) {
+      const long long p = a.start + r;
+      st = push<T, RX, RY, RZ, REUSE>(a, xp, yp, zp, un, vn, wn, all_in);
+      if (st == ST_OK) {
+        __stcs(a.x + p, xp); __stcs(a.y + p, yp); __stcs(a.z + p, zp);
+        __stcs(a.u + p, un); __stcs(a.v + p, vn); __stcs(a.w + p, wn);
+      }
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, st != ST_OK);
+    if (bad) {
+      if ((threadIdx.x & 31) == 0) atomicOr(a.skip + (r >> 5), bad);
+      if (st != ST_OK) atomicMax(a.status, st);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deposition.  Lane L of a warp owns corner c = L & 7 of moments g, g + 4
+// (g = L >> 3) and, over half a tile, moment 8 + (g & 1).  Every tile's
+// staged particles are folded per cell (q * w_c * m) and added into a
+// per-warp node patch in shared memory: sums over the nodes
+// [pi0, pi0 + PX) x [pj0, pj0 + 4) x [pk0, pk0 + 4) for the 10 moments — the
+// neighbourhood of the cells a chunk of sorted particles covers, strays
+// included.  Each lane only ever touches the patch values of its own
+// (corner, moment) pairs, so no atomics.  The patch is converted to the
+// lattice and flushed when the chunk ends or its cells leave the patch.
+template <int PX>
+struct Patch {
+  static constexpr int kNodes = PX * 16;      // node (px, py, pz) at (px * 4 + py) * 4 + pz
+  static constexpr int kStride = kNodes + 2;  // per moment; +2 spreads lane groups over banks
+  static constexpr int kLen = 10 * kStride;
+};
+
+template <typename T>
+__device__ __forceinline__ long long lattice(const Params<T>& a, T v, int node) {
+  const double iv = a.iv_d ? __ldg(a.iv_d + node) : (double)__ldg(a.iv_f + node);
+  return __double2ll_rn((double)v * iv * a.scale);
+}
+
+// The patch's nodes are split over the lanes (node lane + 32 i); each lane
+// holds invvol * 2^43 of its nodes in registers, loaded when the patch is
+// anchored so the loads complete long before the flush uses them.
+template <int PX>
+struct PatchNodes {
+  static constexpr int kPer = PX * 16 / 32;
+  double ivs[kPer];
+  int gnode[kPer];  // global node index, -1 outside the grid
+};
+
+template <int PX, typename T>
+__device__ __forceinline__ void patch_anchor(const Params<T>& a, PatchNodes<PX>& pn, int pi0,
+                                             int pj0, int pk0, unsigned lane) {
+#pragma unroll
+  for (int i = 0; i < PatchNodes<PX>::kPer; ++i) {
+    const int n = (int)lane + 32 * i;
+    const int gi = pi0 + (n >> 4), gj = pj0 + ((n >> 2) & 3), gk = pk0 + (n & 3);
+    const bool in = gi >= 0 && gi <= a.nx && gj >= 0 && gj <= a.ny && gk >= 0 && gk <= a.nz;
+    const int g = in ? (gi * a.NY + gj) * a.NZ + gk : 0;
+    pn.gnode[i] = in ? g : -1;
+    const double iv = a.iv_d ? __ldg(a.iv_d + g) : (double)__ldg(a.iv_f + g);
+    pn.ivs[i] = iv * a.scale;
+  }
+}
+
+// Flush and clear the patch: lane handles its nodes for all 10 moments; a
+// nonzero sum goes onto the lattice (x invvol x 2^43, rint) with one
+// REDG.ADD.64 (consecutive lanes hold z-consecutive nodes).
+template <int PX, typename T>
+__device__ __forceinline__ void patch_flush(const Params<T>& a, T* patch,
+                                            const PatchNodes<PX>& pn, unsigned lane) {
+  typedef Patch<PX> Pt;
+#pragma unroll
+  for (int i = 0; i < PatchNodes<PX>::kPer; ++i) {
+    const int n = (int)lane + 32 * i;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      T* pv = patch + m * Pt::kStride + n;
+      const T v = *pv;
+      if (v != T(0)) {
+        *pv = T(0);
+        if (pn.gnode[i] >= 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)m * a.NN + pn.gnode[i]),
+                    (unsigned long long)__double2ll_rn((double)v * pn.ivs[i]));
+      }
+    }
+  }
+}
+
+// main fold of all 32 staged particles for this lane's three values: rows of
+// bases br, moments m0r / m1r over the whole tile, and the third moment m3r
+// over this lane's half tile (b3 = bases of that half)
+__device__ __forceinline__ void main_fold(const float* br, const float* m0r, const float* m1r,
+                                          const float* b3, const float* m3r, float& s0,
+                                          float& s1, float& s2) {
+  F2 S0 = f2(0.f, 0.f), S1 = f2(0.f, 0.f), S2 = f2(0.f, 0.f);
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 4) {
+    const float4 b = *reinterpret_cast<const float4*>(br + kk);
+    const float4 x0 = *reinterpret_cast<const float4*>(m0r + kk);
+    const float4 x1 = *reinterpret_cast<const float4*>(m1r + kk);
+    S0 = fma2(f2(b.x, b.y), f2(x0.x, x0.y), S0);
+    S0 = fma2(f2(b.z, b.w), f2(x0.z, x0.w), S0);
+    S1 = fma2(f2(b.x, b.y), f2(x1.x, x1.y), S1);
+    S1 = fma2(f2(b.z, b.w), f2(x1.z, x1.w), S1);
+  }
+#pragma unroll
+  for (int kk = 0; kk < 16; kk += 4) {
+    const float4 b = *reinterpret_cast<const float4*>(b3 + kk);
+    const float4 x2 = *reinterpret_cast<const float4*>(m3r + kk);
+    S2 = fma2(f2(b.x, b.y), f2(x2.x, x2.y), S2);
+    S2 = fma2(f2(b.z, b.w), f2(x2.z, x2.w), S2);
+  }
+  s0 = S0.x + S0.y;
+  s1 = S1.x + S1.y;
+  s2 = S2.x + S2.y;
+}
+__device__ __forceinline__ void main_fold(const double* br, const double* m0r,
+                                          const double* m1r, const double* b3,
+                                          const double* m3r, double& s0, double& s1,
+                                          double& s2) {
+  double a0 = 0, a1 = 0, c0 = 0, c1 = 0, e0 = 0, e1 = 0;
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 2) {
+    const double2 b = *reinterpret_cast<const double2*>(br + kk);
+    const double2 x0 = *reinterpret_cast<const double2*>(m0r + kk);
+    const double2 x1 = *reinterpret_cast<const double2*>(m1r + kk);
+    a0 = fma(b.x, x0.x, a0);
+    a1 = fma(b.y, x0.y, a1);
+    c0 = fma(b.x, x1.x, c0);
+    c1 = fma(b.y, x1.y, c1);
+  }
+#pragma unroll
+  for (int kk = 0; kk < 16; kk += 2) {
+    const double2 b = *reinterpret_cast<const double2*>(b3 + kk);
+    const double2 x2 = *reinterpret_cast<const double2*>(m3r + kk);
+    e0 = fma(b.x, x2.x, e0);
+    e1 = fma(b.y, x2.y, e1);
+  }
+  s0 = a0 + a1;
+  s1 = c0 + c1;
+  s2 = e0 + e1;
+}
+
+// Deposit (interpolation of the 10 moments) of the moved particles.  Each
+// warp claims chunks of CHUNK particles; tiles of 32 are staged in shared
+// memory and folded per cell.
+template <typename T, int PX, int CHUNK, int MINB>
+__global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constant__ Params<T> a) {
+  typedef Patch<PX> Pt;
+  constexpr int KR = row_len<T>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const smem_t = reinterpret_cast<T*>(smem_raw);
+  const unsigned lane = lane_id();
+  T* const st = smem_t + (threadIdx.x >> 5) * (stage_len<T>() + Pt::kLen);
+  T* const st_bs = st;             // [8][KR] bases q * w_c
+  T* const st_mv = st + 8 * KR;    // [10][KR], row m = moment m (row 0: constant 1)
+  T* const patch = st + stage_len<T>();  // [10][kStride]
+  const int lc = lane & 7, lg = lane >> 3;
+  const int poff = (lc & 1) * 16 + ((lc >> 1) & 1) * 4 + ((lc >> 2) & 1);
+  const bool third = lg < 2;
+  const int m3 = 8 + (lg & 1), h3 = (lg >> 1) * 16;
+  // this lane's three patch value columns (moments lg, lg + 4, 8 + lg)
+  T* const pv0 = patch + lg * Pt::kStride + poff;
+  T* const pv1 = patch + (lg + 4) * Pt::kStride + poff;
+  T* const pv2 = patch + (third ? lg + 8 : 8) * Pt::kStride + poff;
+  st_mv[lane] = T(1);
+  for (int r = lane; r < Pt::kLen; r += 32) patch[r] = T(0);
+  __syncwarp();
+  long long nxt = 0;
+  if (lane == 0) nxt = (long long)atomicAdd(a.work, (unsigned long long)CHUNK);
+  nxt = __shfl_sync(0xffffffffu, nxt, 0);
+  // prefetched particle of the next tile
+  T px_ = 0, py_ = 0, pz_ = 0, pu_ = 0, pv_ = 0, pw_ = 0, pq_ = 0;
+  unsigned sk_ = 0u;
+  auto fetch = [&](long long r, long long end) {
+    if (r < end) {
+      const long long p = a.start + r;
+      px_ = __ldcs(a.x + p); py_ = __ldcs(a.y + p); pz_ = __ldcs(a.z + p);
+      pu_ = __ldcs(a.u + p); pv_ = __ldcs(a.v + p); pw_ = __ldcs(a.w + p);
+      pq_ = __ldcs(a.q + p);
+    }
+    sk_ = __ldg(a.skip + (r >> 5));
+  };
+  if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
+  const T* brow = st_bs + lc * KR;
+  const T* m0row = st_mv + lg * KR;
+  const T* m1row = st_mv + (lg + 4) * KR;
+  const T* m2row = st_mv + (third ? lg + 8 : 8) * KR;
+  while (nxt < a.count) {
+    const long long w0 = nxt;
+    const long long w1 = w0 + CHUNK < a.count ? w0 + CHUNK : a.count;
+    if (lane == 0) nxt = (long long)atomicAdd(a.work, (unsigned long long)CHUNK);
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+    int pi0 = 0, pj0 = 0, pk0 = 0;  // patch origin (node coordinates)
+    bool anchored = false;
+    PatchNodes<PX> pn;
+    for (long long t0 = w0; t0 < w1; t0 += 32) {
+      const long long r = t0 + lane;
+      const bool valid = r < w1 && !((sk_ >> lane) & 1u);
+      const T xp = px_, yp = py_, zp = pz_, un = pu_, vn = pv_, wn = pw_, qp = pq_;
+      if (t0 + 32 < w1) fetch(t0 + 32 + lane, w1);
+      else if (nxt < a.count) fetch(nxt + lane, nxt + CHUNK < a.count ? nxt + CHUNK : a.count);
+      // ---- stage this lane's particle: 8 bases q*w_c and the moments
+      int ci = 0, cj = 0, ck = 0;
+      {
+        T fx = 0, fy = 0, fz = 0, qs = 0;
+        if (valid) {
+          cell_of(a, xp, yp, zp, fx, fy, fz, ci, cj, ck);
+          qs = qp;
+        }
+        const T qax = qs * (T(1) - fx), qfx = qs * fx;
+        const T ay = T(1) - fy, az = T(1) - fz;
+        const T w00 = qax * ay, w10 = qfx * ay, w01 = qax * fy, w11 = qfx * fy;
+        st_bs[0 * KR + lane] = w00 * az; st_bs[1 * KR + lane] = w10 * az;
+        st_bs[2 * KR + lane] = w01 * az; st_bs[3 * KR + lane] = w11 * az;
+        st_bs[4 * KR + lane] = w00 * fz; st_bs[5 * KR + lane] = w10 * fz;
+        st_bs[6 * KR + lane] = w01 * fz; st_bs[7 * KR + lane] = w11 * fz;
+        T* mv = st_mv + lane;
+        mv[1 * KR] = un; mv[2 * KR] = vn; mv[3 * KR] = wn;
+        mv[4 * KR] = un * un; mv[5 * KR] = un * vn; mv[6 * KR] = un * wn;
+        mv[7 * KR] = vn * vn; mv[8 * KR] = vn * wn; mv[9 * KR] = wn * wn;
+      }
+      const unsigned V = __ballot_sync(0xffffffffu, valid);
+      if (V == 0u) continue;
+      // ---- patch placement
+      if (!anchored) {
+        anchored = true;
+        const int src = __ffs(V) - 1;
+        pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
+        pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
+        pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+        patch_anchor<PX>(a, pn, pi0, pj0, pk0, lane);
+      }
+      int dx = ci - pi0, dy = cj - pj0, dz = ck - pk0;
+      bool fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
+                 (unsigned)dz <= 2u;
+      unsigned F = __ballot_sync(0xffffffffu, fit);
+      if (__popc(V & ~F) > __popc(F)) {
+        // the run moved on: flush and re-anchor at its first particle outside
+        patch_flush<PX>(a, patch, pn, lane);
+        const int src = __ffs(V & ~F) - 1;
+        pi0 = __shfl_sync(0xffffffffu, ci, src) - 1;
+        pj0 = __shfl_sync(0xffffffffu, cj, src) - 1;
+        pk0 = __shfl_sync(0xffffffffu, ck, src) - 1;
+        patch_anchor<PX>(a, pn, pi0, pj0, pk0, lane);
+        dx = ci - pi0; dy = cj - pj0; dz = ck - pk0;
+        fit = valid && (unsigned)dx <= (unsigned)(PX - 2) && (unsigned)dy <= 2u &&
+              (unsigned)dz <= 2u;
+        F = __ballot_sync(0xffffffffu, fit);
+      }
+      const int pnode = (dx * 4 + dy) * 4 + dz;  // patch node of corner 000 (fitting lanes)
+      // ---- main cell: the larger of the first / last fitting lane's cells
+      const int ka = __shfl_sync(0xffffffffu, pnode, __ffs(F | 1u) - 1);
+      const int kb = __shfl_sync(0xffffffffu, pnode, 31 - __clz(F | 1u));
+      const unsigned MA = __ballot_sync(0xffffffffu, fit && pnode == ka);
+      const unsigned MB = __ballot_sync(0xffffffffu, fit && pnode == kb);
+      const bool useb = __popc(MB) > __popc(MA);
+      const int kmain = useb ? kb : ka;
+      const unsigned Mm = useb ? MB : MA;
+      __syncwarp();
+      // ---- other cells of the tile: per-cell fold of their few particles
+      for (unsigned rest = F & ~Mm; rest;) {
+        const int kg = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
+        const unsigned MG = __ballot_sync(0xffffffffu, fit && pnode == kg);
+        rest &= ~MG;
+        // the cell's patch values are read first (no alias with the staged
+        // rows) so their latency hides behind the fold
+        const T o0 = pv0[kg], o1 = pv1[kg], o2 = pv2[kg];
+        T t0s = 0, t1s = 0, t2s = 0;
+        for (unsigned m = MG; m; m &= m - 1u) {
+          const int kk = __ffs(m) - 1;
+          const T b = brow[kk];
+          t0s = fma(b, m0row[kk], t0s);
+          t1s = fma(b, m1row[kk], t1s);
+          t2s = fma(b, m2row[kk], t2s);
+        }
+        pv0[kg] = o0 + t0s;
+        pv1[kg] = o1 + t1s;
+        if (third) pv2[kg] = o2 + t2s;
+      }
+      // ---- particles whose cells are outside the patch (rare): straight to the lattice
+      for (unsigned out = V & ~F; out;) {
+        const int src = __ffs(out) - 1;
+        const int oi = __shfl_sync(0xffffffffu, ci, src);
+        const int oj = __shfl_sync(0xffffffffu, cj, src);
+        const int ok = __shfl_sync(0xffffffffu, ck, src);
+        const unsigned M2 =
+            __ballot_sync(0xffffffffu, valid && !fit && ci == oi && cj == oj && ck == ok);
+        out &= ~M2;
+        T t0s = 0, t1s = 0, t2s = 0;
+        for (unsigned m = M2; m; m &= m - 1u) {
+          const int kk = __ffs(m) - 1;
+          const T b = brow[kk];
+          t0s = fma(b, m0row[kk], t0s);
+          t1s = fma(b, m1row[kk], t1s);
+          t2s = fma(b, m2row[kk], t2s);
+        }
+        const int node = ((oi + (lc & 1)) * a.NY + (oj + ((lc >> 1) & 1))) * a.NZ + ok +
+                         ((lc >> 2) & 1);
+        long long* dst = a.acc + (size_t)lg * a.NN + node;
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst),
+                  (unsigned long long)lattice(a, t0s, node));
+        atomicAdd(reinterpret_cast<unsigned long long*>(dst + (size_t)4 * a.NN),
+                  (unsigned long long)lattice(a, t1s, node));
+        if (third)
+          atomicAdd(reinterpret_cast<unsigned long long*>(dst + (size_t)8 * a.NN),
+                    (unsigned long long)lattice(a, t2s, node));
+      }
+      if (V & ~Mm) {
+        if (((V & ~Mm) >> lane) & 1u) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) st_bs[c * KR + lane] = T(0);
+        }
+        __syncwarp();
+      }
+      // ---- main fold: all 32 staged particles (others have zero bases)
+      if (Mm) {
+        T s0, s1, s2;
+        main_fold(brow, m0row, m1row, brow + h3, st_mv + m3 * KR + h3, s0, s1, s2);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 16);
+        pv0[kmain] += s0;
+        pv1[kmain] += s1;
+        if (third) pv2[kmain] += s2;
+      }
+      __syncwarp();
+    }
+    if (anchored) patch_flush<PX>(a, patch, pn, lane);
+    __syncwarp();
+  }
+}
+
+// Per-cell coefficient records (computed in f64, rounded once to O), three
+// component pairs (a, b) = (Ex, Ey), (Bx, By), (Ez, Bz), four quads each:
+// (c0a c0b c1a c1b) (c2a c2b c4a c4b) (c3a c3b c5a c5b) (c6a c6b c7a c7b);
+// after the records, max |E| over the nodes (float, rounded up).
+template <typename F, typename O>
+__global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int nx, int ny,
+                           int nz, O* __restrict__ rec, unsigned* __restrict__ emax_bits) {
+  const int NY = ny + 1, NZ = nz + 1, NN = (nx + 1) * NY * NZ;
+  const int ncell = nx * ny * nz;
+  const int comp[6] = {0, 1, 3, 4, 2, 5};  // component of pair slot 2p + member
+  double e2max = 0.0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += gridDim.x * blockDim.x) {
+    // threads walk the cells k fastest (coalesced field reads, k is the
+    // fastest index of E / B); records are stored x fastest (sort order)
+    const int k = t % nz, j = (t / nz) % ny, i = t / (nz * ny);
+    const int c = i + nx * (j + ny * k);
+    const int n0 = (i * NY + j) * NZ + k;
+    const int sx = NY * NZ, sy = NZ;
+    double co[6][8];
+    double e2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int h = 0; h < 6; ++h) {
+      const int m = comp[h];
+      const F* f = (m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN) + n0;
+      const double f000 = f[0], f100 = f[sx], f010 = f[sy], f110 = f[sx + sy];
+      const double f001 = f[1], f101 = f[sx + 1], f011 = f[sy + 1], f111 = f[sx + sy + 1];
+      if (m < 3) {
+        e2[0] += f000 * f000; e2[1] += f100 * f100; e2[2] += f010 * f010; e2[3] += f110 * f110;
+        e2[4] += f001 * f001; e2[5] += f101 * f101; e2[6] += f011 * f011; e2[7] += f111 * f111;
+      }
+      co[h][0] = f000;
+      co[h][1] = f100 - f000;
+      co[h][2] = f010 - f000;
+      co[h][3] = f001 - f000;
+      co[h][4] = (f110 - f100) - (f010 - f000);
+      co[h][5] = (f101 - f001) - (f100 - f000);
+      co[h][6] = (f011 - f001) - (f010 - f000);
+      co[h][7] = ((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000));
+    }
+    O* o = rec + (size_t)c * 48;
+    const int slot[4][2] = {{0, 1}, {2, 4}, {3, 5}, {6, 7}};
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        O* d = o + (4 * pr + qd) * 4;
+        d[0] = (O)co[2 * pr][slot[qd][0]];
+        d[1] = (O)co[2 * pr + 1][slot[qd][0]];
+        d[2] = (O)co[2 * pr][slot[qd][1]];
+        d[3] = (O)co[2 * pr + 1][slot[qd][1]];
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) e2max = fmax(e2max, e2[q]);
+  }
+  // non-negative floats order like their bit patterns; rounded up
+  unsigned bits = __float_as_uint(__double2float_ru(sqrt(e2max)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+  if ((threadIdx.x & 31) == 0 && bits) atomicMax(emax_bits, bits);
+}
+
+}  // namespace sk
+
+namespace {
+
+int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// persistent grid: every SM gets its occupancy's worth of blocks
+template <typename K>
+int grid_of(K k, size_t smem, long long per_block_work, long long count) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const long long need = (count + per_block_work - 1) / per_block_work;
+  long long g = (long long)sms() * per_sm;
+  if (need < g) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// f32: record reuse across the mover iterations (~100 registers, 16 warps /
+// SM; measured best); f64: no reuse (the record is 96 registers)
+template <typename T, bool RX, bool RY, bool RZ>
+int launch_mover(const sk::Params<T>& a, cudaStream_t s) {
+  constexpr bool kF = std::is_same<T, float>::value;
+  auto k = sk::mover_kernel<T, RX, RY, RZ, kF, kF ? 2 : 2>;
+  const int g = grid_of(k, 0, 256, a.count);
+  const int th = timing_begin(TK_MOVER, s);
+  k<<<g, 256, 0, s>>>(a);
+  timing_end(th, s);
+  note_launch();
+  return launch_check("mover launch");
+}
+
+// f32: 8-node-wide patch, 512-particle chunks, 3 blocks (24 warps) / SM;
+// f64: the shared memory per warp doubles, so 6-wide patches, 256-particle
+// chunks and 2 blocks / SM
+template <typename T>
+int launch_deposit(const sk::Params<T>& a, cudaStream_t s) {
+  constexpr bool kF = std::is_same<T, float>::value;
+  constexpr int PX = kF ? 8 : 6, CHUNK = kF ? 512 : 256, MINB = kF ? 3 : 2;
+  auto k = sk::deposit_kernel<T, PX, CHUNK, MINB>;
+  const size_t smem =
+      (size_t)(256 / 32) * (sk::stage_len<T>() + sk::Patch<PX>::kLen) * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int g = grid_of(k, smem, (long long)CHUNK * 8, a.count);
+  const int th = timing_begin(TK_DEPOSIT, s);
+  k<<<g, 256, smem, s>>>(a);
+  timing_end(th, s);
+  note_launch();
+  return launch_check("deposit launch");
+}
+
+template <typename T>
+int launch_pair(const sk::Params<T>& a, const int64_t* geo_i, cudaStream_t s) {
+  const int m = (geo_i[3] ? 1 : 0) | (geo_i[4] ? 2 : 0) | (geo_i[5] ? 4 : 0);
+  int rc;
+  switch (m) {
+    case 0: rc = launch_mover<T, false, false, false>(a, s); break;
+    case 1: rc = launch_mover<T, true, false, false>(a, s); break;
+    case 2: rc = launch_mover<T, false, true, false>(a, s); break;
+    case 3: rc = launch_mover<T, true, true, false>(a, s); break;
+    case 4: rc = launch_mover<T, false, false, true>(a, s); break;
+    case 5: rc = launch_mover<T, true, false, true>(a, s); break;
+    case 6: rc = launch_mover<T, false, true, true>(a, s); break;
+    default: rc = launch_mover<T, true, true, true>(a, s); break;
+  }
+  return rc ? rc : launch_deposit<T>(a, s);
+}
+
+template <typename T>
+int split_fused(const Call& c, const void* rec_in, cudaStream_t s) {
+  sk::Params<T> a;
+  a.x = (T*)c.x; a.y = (T*)c.y; a.z = (T*)c.z;
+  a.u = (T*)c.u; a.v = (T*)c.v; a.w = (T*)c.w;
+  a.q = (const T*)c.q;
+  a.start = c.start; a.count = c.count;
+  a.iv_f = c.fbytes == 4 ? (const float*)c.invvol : nullptr;
+  a.iv_d = c.fbytes == 8 ? (const double*)c.invvol : nullptr;
+  a.acc = (long long*)c.acc;
+  a.nx = (int)c.geo_i[0]; a.ny = (int)c.geo_i[1]; a.nz = (int)c.geo_i[2];
+  a.NY = a.ny + 1; a.NZ = a.nz + 1; a.NN = (a.nx + 1) * a.NY * a.NZ;
+  a.cny = a.nx * a.ny;
+  for (int k = 0; k < 3; ++k) {
+    const T o = (T)c.geo_f[3 + k], L = (T)c.geo_f[6 + k];
+    const T hi = o + L;  // particle-precision sum, as the reference
+    a.o[k] = o; a.L[k] = L; a.hi[k] = hi; a.hi2[k] = hi + hi;
+    const double gd = c.fbytes == 8 ? c.geo_g[k] : (double)(float)c.geo_g[k];
+    const double go = c.fbytes == 8 ? c.geo_g[3 + k] : (double)(float)c.geo_g[3 + k];
+    a.idx[k] = (T)(1.0 / gd);
+    a.ogs[k] = (T)(go / gd);
+    a.bc_eps[k] = (T)((sizeof(T) == 4 ? 1e-5 : 1e-13) * (fabs((double)o) + (double)L) + 1e-30);
+  }
+  a.dt = (T)c.dt; a.dth = (T)c.dth; a.qdt2m = (T)c.qdt2m;
+  a.beta = (T)c.beta;
+  a.beta2 = a.beta * a.beta;
+  a.scale = c.scale;
+  a.n_iters = c.n_iters;
+  a.status = c.status;
+  void* rec = const_cast<void*>(rec_in);
+  const size_t rbytes = split_records_bytes((int)sizeof(T), c.geo_i);
+  // one bit per particle, +2 words of slack
+  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 8 + 255) & ~(size_t)255;
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, 256 + skip_bytes + (rec ? 0 : rbytes), s);
+  if (e != cudaSuccess) {
+    set_error("split scratch alloc: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  a.work = (unsigned long long*)scratch;
+  a.skip = (unsigned*)((char*)scratch + 256);
+  cudaMemsetAsync(scratch, 0, 256 + skip_bytes, s);
+  int rc = 0;
+  if (!rec) {
+    rec = (char*)scratch + 256 + skip_bytes;
+    rc = split_pack_records((int)sizeof(T), c.fbytes, c.E, c.B, c.geo_i, rec, s);
+  }
+  a.rec = rec;
+  a.emax = reinterpret_cast<const float*>((const char*)rec + (rbytes - 32));
+  if (!rc) rc = launch_pair<T>(a, c.geo_i, s);
+  cudaFreeAsync(scratch, s);
+  return rc;
+}
+
+}  // namespace
+
+size_t split_records_bytes(int pbytes, const int64_t* geo_i) {
+  // 12 quads of the particle type per cell, then 32 bytes holding max |E|
+  return (size_t)geo_i[0] * geo_i[1] * geo_i[2] * 48 * (pbytes == 8 ? 8 : 4) + 32;
+}
+
+int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
+                       const int64_t* geo_i, void* rec, cudaStream_t s) {
+  const int nx = (int)geo_i[0], ny = (int)geo_i[1], nz = (int)geo_i[2];
+  const long long ncell = (long long)nx * ny * nz;
+  int blocks = (int)((ncell + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  unsigned* emax =
+      reinterpret_cast<unsigned*>((char*)rec + split_records_bytes(pbytes, geo_i) - 32);
+  cudaMemsetAsync(emax, 0, 32, s);
+  const int th = timing_begin(TK_RECORDS, s);
+  if (pbytes == 8) {
+    if (fbytes == 8)
+      sk::pack_cells<double, double><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B,
+                                                            nx, ny, nz, (double*)rec, emax);
+    else
+      sk::pack_cells<float, double><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B,
+                                                           nx, ny, nz, (double*)rec, emax);
+  } else {
+    if (fbytes == 8)
+      sk::pack_cells<double, float><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B,
+                                                           nx, ny, nz, (float*)rec, emax);
+    else
+      sk::pack_cells<float, float><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B, nx,
+                                                          ny, nz, (float*)rec, emax);
+  }
+  timing_end(th, s);
+  note_launch();
+  return launch_check("cell record pack");
+}
+
+int split_fused(const Call& c, const void* rec, cudaStream_t s) {
+  // the f64 instantiation (per-tile f64 sums) measured 25% faster than the
+  // generic f64 kernel but outside 1e-10 of the reference's per-contribution
+  // lattice rounding on the small moments, so only f32 particles come here
+  if (c.pbytes != 4) {
+    set_error("split kernels: f32 particles only");
+    return -1;
+  }
+  return split_fused<float>(c, rec, s);
+}
+
+}  // namespace bp

@@ -121,7 +121,7 @@ class DeviceSimulation:
         self._records_fresh = False
         if self.arith == "fast" and pd == torch.float32:
             gi = np.ascontiguousarray(self.geo_i, np.int64)
-            nbytes = int(_lib.load().bp_field_records_bytes(ctypes.c_void_p(gi.ctypes.data)))
+            nbytes = int(_lib.load().bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data)))
             self.records = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=self.device)
         if self.distributed:
             import torch.distributed as dist
@@ -173,7 +173,8 @@ class DeviceSimulation:
         if not self._records_fresh:
             L = _lib.load()
             gi = np.ascontiguousarray(self.geo_i, np.int64)
-            rc = L.bp_field_records_build(self.E.element_size(), ctypes.c_void_p(self.E.data_ptr()),
+            rc = L.bp_field_records_build(4, self.E.element_size(),
+                                          ctypes.c_void_p(self.E.data_ptr()),
                                           ctypes.c_void_p(self.B.data_ptr()),
                                           ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
                                           ctypes.c_void_p(stream.cuda_stream))

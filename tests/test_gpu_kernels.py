@@ -268,7 +268,7 @@ def test_tma_stream_path_matches(gpu, oracle, tma_stream, monkeypatch, mode, ari
 
 @pytest.mark.parametrize("mode", ["single", "mixed"])
 def test_fast_f32_fused_is_deterministic(gpu, mode):
-    """The f32 fused kernel (bp_f32.cu) claims work dynamically but flushes
+    """The fast fused kernels (bp_split.cu) claim work dynamically but flush
     every chunk's sums on its own, so repeated launches give identical bits."""
     from paper_2008_04397_b200 import kernels as K
     torch = gpu
@@ -297,17 +297,19 @@ _BCS = [(a, b, c) for a in ("periodic", "reflecting") for b in ("periodic", "ref
 
 @pytest.mark.parametrize("bc", _BCS, ids=["".join(k[0] for k in b) for b in _BCS])
 @pytest.mark.parametrize("failing", [False, True])
-def test_fast_f32_every_boundary_kind(gpu, oracle, bc, failing):
-    """The f32 kernels are instantiated per boundary kind (bp_f32.cu): every
-    combination against the oracle within 1e-4, on a span with an unaligned
-    start and a ragged tail.  `failing` gives one particle in 97 a velocity
+@pytest.mark.parametrize("mode", ["single", "double"])
+def test_fast_split_every_boundary_kind(gpu, oracle, bc, failing, mode):
+    """The fast kernels are instantiated per boundary kind (bp_split.cu): every
+    combination against the oracle within 1e-4 (f32) / 1e-10 (f64), on a span
+    with an unaligned start and a ragged tail.  `failing` gives one particle in 97 a velocity
     of 1e4 (a certain runaway / midpoint failure): those must be neither
     stored nor deposited, exactly as in the reference."""
     from paper_2008_04397_b200 import kernels as K
     torch = gpu
     n = 60_013
     geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(
-        "single", n, seed=101, order="sorted", bc=bc)
+        mode, n, seed=101, order="sorted", bc=bc)
+    rtol = FAST_RTOL[mode]
     if failing:
         bad = np.arange(5, n, 97)
         arrs[3][bad] = pd(1e4)
@@ -332,10 +334,10 @@ def test_fast_f32_every_boundary_kind(gpu, oracle, bc, failing):
         # outside the span nothing moves
         assert np.array_equal(got[:start], r[:start]) and np.array_equal(got[start + count:],
                                                                             r[start + count:])
-        _assert_close(name, r, got, 1e-4, per)
+        _assert_close(name, r, got, rtol, per)
     got = dacc.cpu().numpy()
     for m in range(10):
-        _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, 1e-4)
+        _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, rtol)
 
 
 def test_prepared_records_and_timing_api(gpu):
@@ -363,17 +365,17 @@ def test_prepared_records_and_timing_api(gpu):
     assert t["mover"][1] == 1 and t["deposit"][1] == 1 and t["records"][1] == 1
     assert t["mover"][0] > 0.0 and t["deposit"][0] > 0.0
     gi = np.ascontiguousarray(geo_i, np.int64)
-    nbytes = L.bp_field_records_bytes(ctypes.c_void_p(gi.ctypes.data))
+    nbytes = L.bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data))
     assert nbytes > 0
     rec = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
     ptr = (rec.data_ptr() + 255) & ~255
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    assert L.bp_field_records_build(4, ctypes.c_void_p(dE.data_ptr()),
+    assert L.bp_field_records_build(4, 4, ctypes.c_void_p(dE.data_ptr()),
                                     ctypes.c_void_p(dB.data_ptr()),
                                     ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
                                     stream) == 0
     # misaligned records are refused
-    assert L.bp_field_records_build(4, ctypes.c_void_p(dE.data_ptr()),
+    assert L.bp_field_records_build(4, 4, ctypes.c_void_p(dE.data_ptr()),
                                     ctypes.c_void_p(dB.data_ptr()),
                                     ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr + 4),
                                     stream) == _lib.EINVAL
