@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file gpurun_out/launches_$R.csv \
     python bench.py --steps 10 --warmup 0 --no-e2e --no-cpu --no-parity > gpurun_out/launches_$R.log 2>&1
 for K in mover deposit; do
-  ncu --set full --clock-control none --import-source on -k regex:sk::${K}_kernel -s 20 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:${K}_kernel -s 20 -c 1 \
       -o gpurun_out/${K}_f32_$R python bench.py --steps 6 --warmup 0 --no-e2e --no-cpu --no-parity \
       > gpurun_out/${K}_f32_$R.log 2>&1
 done
