@@ -1,6 +1,6 @@
 """Out-of-core path (BASELINE.json configs[3]): a population held in pinned
 host memory is streamed through the device every step by the C ABI's
-bp_fused_span_host (double-buffered batches on two CUDA streams), with the
+bp_fused_span_host (three batches in flight on three CUDA streams), with the
 device working set capped by a byte budget (the reference's ByteBudget,
 pipeline.py:47-77).  Reported against the measured host<->device link.
 
@@ -70,8 +70,8 @@ accs = [np.zeros((10,) + geom.node_shape, np.int64) for _ in species]
 geo_f, geo_i = make_geo_arrays(geom, np.float32)
 gf = np.ascontiguousarray(geo_f, np.float64)
 gi = np.ascontiguousarray(geo_i, np.int64)
-# two slots x 7 arrays x batch x 4 B within the budget (fields / acc aside)
-batch = min(int(args.budget_gb * 1e9 / (2 * 7 * 4)), 1 << 25)  # >= ~16 batches/species keep the 2-deep pipeline full
+# three slots x 7 arrays x batch x 4 B within the budget (fields / acc aside)
+batch = min(int(args.budget_gb * 1e9 / (3 * 7 * 4)), 1 << 25)  # >= ~16 batches/species keep the pipeline full
 hp = lambda a: ctypes.c_void_p(a.ctypes.data)
 tp = lambda t: ctypes.c_void_p(t.data_ptr())
 arith = _lib.ARITH_FAST if args.arith == "fast" else _lib.ARITH_PARITY
