@@ -568,14 +568,25 @@ __global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constan
         // the cell's patch values are read first (no alias with the staged
         // rows) so their latency hides behind the fold
         const T o0 = pv0[kg], o1 = pv1[kg], o2 = pv2[kg];
+        // members software-pipelined: the next member's loads are issued
+        // before this member's products
+        unsigned m = MG;
+        int kk = __ffs(m) - 1;
+        m &= m - 1u;
+        T b = brow[kk], x0 = m0row[kk], x1 = m1row[kk], x2 = m2row[kk];
         T t0s = 0, t1s = 0, t2s = 0;
-        for (unsigned m = MG; m; m &= m - 1u) {
-          const int kk = __ffs(m) - 1;
-          const T b = brow[kk];
-          t0s = fma(b, m0row[kk], t0s);
-          t1s = fma(b, m1row[kk], t1s);
-          t2s = fma(b, m2row[kk], t2s);
+        while (m) {
+          const int kn = __ffs(m) - 1;
+          m &= m - 1u;
+          const T bn = brow[kn], y0 = m0row[kn], y1 = m1row[kn], y2 = m2row[kn];
+          t0s = fma(b, x0, t0s);
+          t1s = fma(b, x1, t1s);
+          t2s = fma(b, x2, t2s);
+          b = bn; x0 = y0; x1 = y1; x2 = y2;
         }
+        t0s = fma(b, x0, t0s);
+        t1s = fma(b, x1, t1s);
+        t2s = fma(b, x2, t2s);
         pv0[kg] = o0 + t0s;
         pv1[kg] = o1 + t1s;
         if (third) pv2[kg] = o2 + t2s;
