@@ -755,10 +755,8 @@ int launch_mover(const sk::Params<T>& a, cudaStream_t s) {
 // f32: 8-node-wide patch, 512-particle chunks, 3 blocks (24 warps) / SM;
 // f64: the shared memory per warp doubles, so 6-wide patches, 256-particle
 // chunks and 2 blocks / SM
-template <typename T>
-int launch_deposit(const sk::Params<T>& a, cudaStream_t s) {
-  constexpr bool kF = std::is_same<T, float>::value;
-  constexpr int PX = kF ? 8 : 6, CHUNK = kF ? 512 : 256, MINB = kF ? 3 : 2;
+template <typename T, int PX, int CHUNK, int MINB>
+int launch_deposit_cfg(const sk::Params<T>& a, cudaStream_t s) {
   auto k = sk::deposit_kernel<T, PX, CHUNK, MINB>;
   const size_t smem =
       (size_t)(256 / 32) * (sk::stage_len<T>() + sk::Patch<PX>::kLen) * sizeof(T);
@@ -773,6 +771,20 @@ int launch_deposit(const sk::Params<T>& a, cudaStream_t s) {
   timing_end(th, s);
   note_launch();
   return launch_check("deposit launch");
+}
+
+// f32: 8-node-wide patch, 512-particle chunks, 3 blocks (24 warps) / SM;
+// f64: the shared memory per warp doubles, so 6-wide patches, 256-particle
+// chunks and 2 blocks / SM
+template <typename T>
+int launch_deposit(const sk::Params<T>& a, cudaStream_t s) {
+  // (measured: 6-wide patches with 256-particle chunks at 24 or 32 warps / SM
+  // are 3-4% slower)
+  if constexpr (std::is_same<T, float>::value) {
+    return launch_deposit_cfg<T, 8, 512, 3>(a, s);
+  } else {
+    return launch_deposit_cfg<T, 6, 256, 2>(a, s);
+  }
 }
 
 template <typename T>
