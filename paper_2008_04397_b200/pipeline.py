@@ -155,10 +155,24 @@ class DeviceSimulation:
     def set_fields(self, E=None, B=None):
         """Phase 1: host E/B (numpy, rank 0) -> HBM, broadcast to all ranks
         (collective: all ranks call it; only rank 0's arrays are used)."""
-        if E is not None:
-            self.E.copy_(self.torch.from_numpy(np.ascontiguousarray(E)), non_blocking=False)
-        if B is not None:
-            self.B.copy_(self.torch.from_numpy(np.ascontiguousarray(B)), non_blocking=False)
+        # staged through persistent pinned buffers: one DMA each, in stream
+        # order, no pageable bounce copy
+        for name, src in (("E", E), ("B", B)):
+            if src is None:
+                continue
+            dst = getattr(self, name)
+            stage = self._pinned(f"_stage_{name}", dst)
+            done = getattr(self, f"_stage_{name}_done", None)
+            if done is not None:
+                done.synchronize()  # the previous DMA out of this buffer
+            if isinstance(src, np.ndarray):
+                stage.numpy()[...] = src
+            else:
+                stage.copy_(src)
+            dst.copy_(stage, non_blocking=True)
+            done = self.torch.cuda.Event()
+            done.record(self.torch.cuda.current_stream(self.device))
+            setattr(self, f"_stage_{name}_done", done)
         if self.distributed:
             broadcast_fields(self.E, self.B, src=0, group=self.group)
         self._records_fresh = False
@@ -270,8 +284,27 @@ class DeviceSimulation:
                                         ctypes.c_void_p(s.cuda_stream))
             _lib.check(rc, "fold_periodic")
 
-    def moments_host(self):
-        return [a.cpu().numpy() for a in self.acc]
+    def _pinned(self, attr, like):
+        """Persistent pinned host tensor shaped like ``like`` (lazily made)."""
+        t = getattr(self, attr, None)
+        if t is None or t.shape != like.shape or t.dtype != like.dtype:
+            t = self.torch.empty(like.shape, dtype=like.dtype, pin_memory=True)
+            setattr(self, attr, t)
+        return t
+
+    def moments_host(self, reuse=False):
+        """The per-species int64 moment grids on the host.  ``reuse=True``
+        returns views of persistent pinned buffers (one DMA each, overwritten
+        by the next call) instead of fresh arrays."""
+        if not reuse:
+            return [a.cpu().numpy() for a in self.acc]
+        out = []
+        for sid, a in enumerate(self.acc):
+            h = self._pinned(f"_mom_host_{sid}", a)
+            h.copy_(a, non_blocking=True)
+            out.append(h)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        return [h.numpy() for h in out]
 
     def total_moments(self):
         """Exact int64 sum of the species grids on device (fields.total_moments)."""
