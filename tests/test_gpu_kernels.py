@@ -297,7 +297,7 @@ _BCS = [(a, b, c) for a in ("periodic", "reflecting") for b in ("periodic", "ref
 
 @pytest.mark.parametrize("bc", _BCS, ids=["".join(k[0] for k in b) for b in _BCS])
 @pytest.mark.parametrize("failing", [False, True])
-@pytest.mark.parametrize("mode", ["single", "double"])
+@pytest.mark.parametrize("mode", ["single", "mixed", "double"])
 def test_fast_split_every_boundary_kind(gpu, oracle, bc, failing, mode):
     """The fast kernels are instantiated per boundary kind (bp_split.cu): every
     combination against the oracle within 1e-4 (f32) / 1e-10 (f64), on a span
@@ -310,13 +310,14 @@ def test_fast_split_every_boundary_kind(gpu, oracle, bc, failing, mode):
     geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state(
         mode, n, seed=101, order="sorted", bc=bc)
     rtol = FAST_RTOL[mode]
+    mixed = 1 if pd != fd else 0
     if failing:
         bad = np.arange(5, n, 97)
         arrs[3][bad] = pd(1e4)
         arrs[4][bad[::2]] = pd(-1e4)
     inv = geom.inv_node_volume(fd)
     tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
-            fd(SCALE), 0)
+            fd(SCALE), mixed)
     start, count = 77, n - 77 - 5
     ref = [a.copy() for a in arrs]
     acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
@@ -392,3 +393,39 @@ def test_prepared_records_and_timing_api(gpu):
     assert st2 == st1
     assert torch.equal(acc1, acc2)
     assert all(torch.equal(a, b) for a, b in zip(d1, d2))
+
+
+
+@pytest.mark.parametrize("count", [0, 1, 5, 31, 33, 511, 513])
+def test_fast_split_tiny_spans(gpu, oracle, count):
+    """Spans shorter than a tile, a chunk or a warp round, at an odd start."""
+    from paper_2008_04397_b200 import kernels as K
+    torch = gpu
+    n = 2_000
+    geom, arrs, E, B, geo_f, geo_g, geo_i, sc, pd, fd = _random_state("single", n, seed=3,
+                                                                       order="sorted")
+    inv = geom.inv_node_volume(fd)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+            fd(SCALE), 0)
+    start = 13
+    ref = [a.copy() for a in arrs]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    st_ref = oracle.fused_span(*ref, start, count, E, B, acc_ref, inv, *tail)
+    d = _dev(torch, arrs)
+    dE, dB, dinv = _dev(torch, [E, B, inv])
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    st = K.fused_span(*d, start, count, dE, dB, dacc, dinv, *tail, arith="fast")
+    assert st == st_ref
+    for name, r, t in zip("xyzuvw", ref, d):
+        got = t.cpu().numpy()
+        assert np.array_equal(got[:start], r[:start])
+        assert np.array_equal(got[start + count:], r[start + count:])
+        if count:
+            _assert_close(name, r[start:start + count], got[start:start + count], 1e-4,
+                          geom.Lx if name == "x" else (geom.Lz if name == "z" else None))
+    got = dacc.cpu().numpy()
+    if count == 0:
+        assert not got.any()
+    for m in range(10):
+        if count:
+            _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, 1e-4)
