@@ -275,12 +275,18 @@ __device__ __forceinline__ int push(const Params<T>& a, T& xp, T& yp, T& zp, T& 
 // the SM holds enough warps to hide the latency of the dependent gather +
 // rotation steps.  Particles that fail (kernels.py:618-621, 672-676) are not
 // stored; their bit in `skip` keeps them out of the deposit.
-template <typename T, bool RX, bool RY, bool RZ, bool REUSE, int MINB>
+template <typename T, bool RX, bool RY, bool RZ, bool REUSE, int MINB, int WCH>
 __global__ void __launch_bounds__(256, MINB) mover_kernel(const __grid_constant__ Params<T> a) {
-  // persistent grid: each thread walks particles r, r + stride, ... with the
-  // next particle's loads in flight while the current one is pushed
-  const long long stride = (long long)gridDim.x * 256;
-  long long r = (long long)blockIdx.x * 256 + threadIdx.x;
+  // persistent grid; each warp walks chunks of WCH consecutive 32-particle
+  // tiles (chunks gw, gw + nw, ...), so the cell records its first tile loads
+  // are L1-hot for the following tiles of the same cells; the next tile's
+  // loads are in flight while this one is pushed
+  const unsigned lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const long long nw = (long long)gridDim.x * 8;
+  constexpr long long CH = 32LL * WCH;
+  long long c = gw;
+  int ti = 0;
   T n1[6] = {0, 0, 0, 0, 0, 0};
   auto fetch = [&](long long rr) {
     if (rr < a.count) {
@@ -289,13 +295,17 @@ __global__ void __launch_bounds__(256, MINB) mover_kernel(const __grid_constant_
       n1[3] = __ldcs(a.u + p); n1[4] = __ldcs(a.v + p); n1[5] = __ldcs(a.w + p);
     }
   };
-  fetch(r);
+  fetch(c * CH + lane);
   // |qdt2m| max|E| (+1e-5 relative slack for the coefficient rounding)
   const T qe = fabs(a.qdt2m) * (T)__ldg(a.emax) * T(1.00001);
-  const long long rbase = r - (threadIdx.x & 31);  // warp-uniform loop bound
-  for (long long rb = rbase; rb < a.count; rb += stride, r += stride) {
+  for (long long base = c * CH; base < a.count; base = c * CH + 32LL * ti) {
+    const long long r = base + lane;
     T xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
-    fetch(r + stride);
+    if (++ti == WCH) {
+      ti = 0;
+      c += nw;
+    }
+    fetch(c * CH + 32LL * ti + lane);
     int st = ST_OK;
     // warp-uniform: the whole warp takes the boundary-free push when it can
     const bool all_in =
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(256, MINB) mover_kernel(const __grid_constant_
     }
     const unsigned bad = __ballot_sync(0xffffffffu, st != ST_OK);
     if (bad) {
-      if ((threadIdx.x & 31) == 0) atomicOr(a.skip + (r >> 5), bad);
+      if (lane == 0) atomicOr(a.skip + (r >> 5), bad);
       if (st != ST_OK) atomicMax(a.status, st);
     }
   }
@@ -738,18 +748,30 @@ int grid_of(K k, size_t smem, long long per_block_work, long long count) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// f32: record reuse across the mover iterations (~100 registers, 16 warps /
-// SM; measured best); f64: no reuse (the record is 96 registers)
-template <typename T, bool RX, bool RY, bool RZ>
-int launch_mover(const sk::Params<T>& a, cudaStream_t s) {
+template <typename T, bool RX, bool RY, bool RZ, int WCH>
+int launch_mover_w(const sk::Params<T>& a, cudaStream_t s) {
   constexpr bool kF = std::is_same<T, float>::value;
-  auto k = sk::mover_kernel<T, RX, RY, RZ, kF, kF ? 2 : 2>;
+  auto k = sk::mover_kernel<T, RX, RY, RZ, kF, 2, WCH>;
   const int g = grid_of(k, 0, 256, a.count);
   const int th = timing_begin(TK_MOVER, s);
   k<<<g, 256, 0, s>>>(a);
   timing_end(th, s);
   note_launch();
   return launch_check("mover launch");
+}
+
+// f32: record reuse across the mover iterations (~100 registers, 16 warps /
+// SM; measured best); f64: no reuse (the record is 96 registers)
+template <typename T, bool RX, bool RY, bool RZ>
+int launch_mover(const sk::Params<T>& a, cudaStream_t s) {
+  static int wch = -1;
+  if (wch < 0) {
+    const char* e = getenv("BP_MOVER_WCH");
+    wch = e ? atoi(e) : 4;
+  }
+  // tiles per warp chunk (measured: 1 -> 1.30 ms, 4 -> 1.27, 8 / 16 -> 1.27)
+  if (wch == 1) return launch_mover_w<T, RX, RY, RZ, 1>(a, s);
+  return launch_mover_w<T, RX, RY, RZ, 4>(a, s);
 }
 
 // f32: 8-node-wide patch, 512-particle chunks, 3 blocks (24 warps) / SM;
