@@ -459,7 +459,8 @@ def e2e_leg(args, sim, species, prec, geom, dist, dev, n_total):
                                       hp(E), hp(B), hp(accs[sid]), hp(inv), hp(sim.geo_f),
                                       hp(sim.geo_g), hp(sim.geo_i), float(sc["dt"]),
                                       float(sc["dth"]), float(sc["qdt2m"]), float(sc["beta"]),
-                                      float(sc["one"]), s.mover_iters, sim.scale, sim.mixed, 0)
+                                      float(sc["one"]), s.mover_iters, sim.scale, sim.mixed,
+                                      int(os.environ.get("BP_HOST_BATCH", "0")))
             _lib.check(rc, "bp_fused_span_host")
 
     one_step()  # warm-up (allocations)

@@ -502,7 +502,7 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
   std::lock_guard<std::mutex> lock(g_host_mu);
   HostCtx& h = g_host;
   const int64_t nn = (geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
-  int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 22);
+  int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 21);
   if (batch > count) batch = count;
   rc = host_ctx_reserve(h, (size_t)batch * pbytes, (size_t)3 * nn * fbytes,
                         (size_t)10 * nn * sizeof(int64_t));
