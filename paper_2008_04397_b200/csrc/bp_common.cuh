@@ -82,6 +82,10 @@ struct SpanParams {
   int bulk;
   // dynamic work distribution: next unclaimed particle of the span
   unsigned long long* work;
+  // two-pass fused span (push-only then deposit-only launch): one bit per
+  // span particle whose push failed — set by the push pass, skipped by the
+  // deposit pass (NULL: not used)
+  unsigned* skip;
 };
 
 // particles per dynamically claimed chunk (32 tiles of a warp)
@@ -515,6 +519,7 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
     const int stg = it & 1;
     const i64 r = t0 + lane;
     bool valid = r < w1;
+    if (!DO_PUSH && a.skip) valid = valid && !((__ldg(a.skip + (t0 >> 5)) >> lane) & 1u);
     const i64 p = a.start + r;
     const bool cur_full = full(t0);
     if (full(t0 + 32)) {
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
       un = __ldcs(a.u + p); vn = __ldcs(a.v + p); wn = __ldcs(a.w + p);
       if (DO_DEPOSIT) qp = __ldcs(a.q + p);
     }
+    bool failed = false;
     if (DO_PUSH) {
       if (valid) {
         const int st = Pol::push(a, K, xp, yp, zp, un, vn, wn);
@@ -545,6 +551,7 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
           // store writes the tile's loaded values back unchanged
           worst = st > worst ? st : worst;
           valid = false;
+          failed = true;
         } else if (cur_full) {
           cur[0 * 32 + lane] = xp; cur[1 * 32 + lane] = yp; cur[2 * 32 + lane] = zp;
           cur[3 * 32 + lane] = un; cur[4 * 32 + lane] = vn; cur[5 * 32 + lane] = wn;
@@ -561,6 +568,10 @@ __global__ void __launch_bounds__(256, BP_MIN_BLOCKS)
             bulk_store(arr[k] + a.start + t0, cur + k * 32, tile_bytes);
           bulk_commit();
         }
+      }
+      if (a.skip) {
+        const unsigned fb = __ballot_sync(0xffffffffu, failed);
+        if (fb && lane == 0) atomicOr(a.skip + (t0 >> 5), fb);
       }
     }
     if (DO_DEPOSIT) {

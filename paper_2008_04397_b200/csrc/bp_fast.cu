@@ -11,7 +11,9 @@ template <typename P, typename F>
 int dispatch(const Call& c, cudaStream_t s) {
   typedef FastPolicy<P, F> Pol;
   switch (c.op) {
-    case OP_FUSED: return run_span<Pol, true, true>(c, true, s);
+    case OP_FUSED:
+      return two_pass_requested() ? run_two_pass<Pol>(c, true, s)
+                                  : run_span<Pol, true, true>(c, true, s);
     case OP_PUSH: return run_span<Pol, true, false>(c, true, s);
     case OP_DEPOSIT: return run_span<Pol, false, true>(c, true, s);
   }

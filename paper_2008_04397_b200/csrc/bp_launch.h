@@ -26,6 +26,7 @@ struct Call {
   void* out;    // gather rows
   int* status;  // device int, atomicMax
   const void* records;  // prebuilt cell records (bp_field_records_build) or NULL
+  unsigned* skip;       // two-pass fused span: failed-push bitmask (internal)
 };
 
 // Return 0 on a successful enqueue, else a negative BP_E* code.

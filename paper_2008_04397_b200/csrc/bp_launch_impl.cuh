@@ -57,6 +57,7 @@ SpanParams<P, F> make_params(const Call& c) {
   a.d.beta2 = (double)a.beta2; a.d.scale = (double)a.scale;
   a.iv_max = nullptr;
   a.work = nullptr;
+  a.skip = c.skip;
   {
     // TMA bulk tiles need every full tile 16-byte aligned in all 7 arrays
     const void* ptrs[7] = {c.x, c.y, c.z, c.u, c.v, c.w, c.q};
@@ -125,7 +126,8 @@ int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t c
   constexpr size_t kFull =
       (size_t)(kThreads / 32) * warp_smem_doubles<typename Pol::P>() * sizeof(double);
   constexpr size_t kStageOnly = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
-  const size_t smem = a.bulk ? kFull : kStageOnly;
+  // a push-only launch without TMA tiles touches no shared memory
+  const size_t smem = a.bulk ? kFull : (DEP ? kStageOnly : 0);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFull);
@@ -170,6 +172,41 @@ int run_span(const Call& c, bool prescale_ok, cudaStream_t s) {
     rc = launch_span<Pol, PUSH, DEP, false>(a, c.count, s);
   cudaFreeAsync(fn, s);
   return rc;
+}
+
+// Fused span as two launches of the generic kernel — push-only (high
+// occupancy, no deposit staging) then deposit-only — with a bitmask of the
+// particles whose push failed so they are not deposited (kernels.py:618-621).
+// Same arithmetic as the one-pass kernel, and the deposit's exact integer sums
+// make the moments identical.
+template <class Pol>
+int run_two_pass(const Call& c0, bool prescale_ok, cudaStream_t s) {
+  Call c = c0;
+  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 8 + 255) & ~(size_t)255;
+  unsigned* skip = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&skip, skip_bytes, s);
+  if (e != cudaSuccess) {
+    set_error("skip bitmask alloc: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  cudaMemsetAsync(skip, 0, skip_bytes, s);
+  c.skip = skip;
+  c.apply_bc = 1;
+  int rc = run_span<Pol, true, false>(c, prescale_ok, s);
+  if (!rc) rc = run_span<Pol, false, true>(c, prescale_ok, s);
+  cudaFreeAsync(skip, s);
+  return rc;
+}
+
+// default on (measured at C3: parity single +1%, f64 fast +4%);
+// BP_GENERIC_TWO_PASS=0 selects the one-pass fused kernel
+inline bool two_pass_requested() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BP_GENERIC_TWO_PASS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 }  // namespace

@@ -34,7 +34,9 @@ int dispatch(const Call& c, cudaStream_t s) {
   // (base*m)*scale == (base*scale)*m exactly only for a power-of-two scale
   const bool pre = is_pow2(c.scale);
   switch (c.op) {
-    case OP_FUSED: return run_span<Pol, true, true>(c, pre, s);
+    case OP_FUSED:
+      return two_pass_requested() ? run_two_pass<Pol>(c, pre, s)
+                                  : run_span<Pol, true, true>(c, pre, s);
     case OP_PUSH: return run_span<Pol, true, false>(c, pre, s);
     case OP_DEPOSIT: return run_span<Pol, false, true>(c, pre, s);
     case OP_GATHER: return run_gather<P, F>(c, s);
