@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "bp_launch.h"
@@ -145,6 +146,116 @@ __global__ void gather_perm8(const T* __restrict__ x, const T* __restrict__ y,
     }
     if (id) oid[r] = id[j];
   }
+}
+
+// One group of the gather: up to 4 same-type arrays and optionally the ids,
+// one block per 1024 destinations with no grid stride, so resident blocks
+// sweep the destination in order and the sources they touch (a particle
+// moves at most a few cells between sorts) stay in a window of about three
+// z-planes of the source arrays.  Gathering the arrays in groups keeps that
+// window (bytes per particle of the group x plane size) inside L2; all eight
+// arrays at once overflow it and every moved particle costs a full sector.
+template <typename T>
+struct GatherGroup {
+  const T* src[4];
+  T* dst[4];
+  int na;
+  const long long* sid;
+  long long* did;
+};
+
+__device__ __forceinline__ uint64_t keep_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float ld_keep(const float* a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ long long ld_keep(const long long* a, uint64_t pol) {
+  long long v;
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_group(GatherGroup<T> g,
+                                                    const uint32_t* __restrict__ order,
+                                                    int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = 4 * t;
+  if (r0 + 4 <= n) {
+    const uint4 j = __ldcs(reinterpret_cast<const uint4*>(order) + t);
+    const uint64_t pol = keep_policy();
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      if (a >= g.na) break;
+      const T* sa = g.src[a];
+      store4(g.dst[a] + r0, ld_keep(sa + j.x, pol), ld_keep(sa + j.y, pol),
+             ld_keep(sa + j.z, pol), ld_keep(sa + j.w, pol));
+    }
+    if (g.sid) {
+      longlong2* di = reinterpret_cast<longlong2*>(g.did + r0);
+      __stcs(di, make_longlong2(ld_keep(g.sid + j.x, pol), ld_keep(g.sid + j.y, pol)));
+      __stcs(di + 1, make_longlong2(ld_keep(g.sid + j.z, pol), ld_keep(g.sid + j.w, pol)));
+    }
+  } else {
+    for (int64_t r = r0; r < n; ++r) {
+      const uint32_t j = order[r];
+      for (int a = 0; a < g.na; ++a) g.dst[a][r] = g.src[a][j];
+      if (g.sid) g.did[r] = g.sid[j];
+    }
+  }
+}
+
+int check(cudaError_t e, const char* what);
+
+// the eight arrays in `groups` passes (1: all at once through gather_perm8)
+template <typename T>
+int gather_grouped(const void* const* src, const void* src_ids, void* const* dst, void* dst_ids,
+                   const uint32_t* order, int64_t n, int groups, cudaStream_t s) {
+  // arrays 0..6 (q may be null) then ids
+  static const int kSplit2[] = {0, 4, 7};
+  static const int kSplit3[] = {0, 3, 6, 7};
+  const int* cut = groups == 2 ? kSplit2 : kSplit3;
+  const int ng = groups == 2 ? 2 : 3;
+  const unsigned blocks = (unsigned)((n + 1023) / 1024);
+  for (int gi = 0; gi < ng; ++gi) {
+    GatherGroup<T> g{};
+    g.na = 0;
+    for (int a = cut[gi]; a < cut[gi + 1]; ++a) {
+      if (!src[a]) continue;
+      g.src[g.na] = static_cast<const T*>(src[a]);
+      g.dst[g.na] = static_cast<T*>(dst[a]);
+      ++g.na;
+    }
+    if (gi == ng - 1 && src_ids) {
+      g.sid = static_cast<const long long*>(src_ids);
+      g.did = static_cast<long long*>(dst_ids);
+    }
+    if (!g.na && !g.sid) continue;
+    gather_group<T><<<blocks, 256, 0, s>>>(g, order, n);
+    note_launch();
+    const int rc = check(cudaGetLastError(), "gather_group");
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int gather_groups_env() {
+  static int g = [] {
+    const char* e = getenv("BP_GATHER_GROUPS");
+    const int v = e ? atoi(e) : 3;
+    return v == 1 || v == 2 ? v : 3;
+  }();
+  return g;
 }
 
 // fold one periodic axis of a (rows, NX, NY, NZ) grid: first += last; last = first
@@ -375,7 +486,11 @@ int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* cons
     rc = check(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k_in, k_out, i_in, i_out, n,
                                                0, end_bit, s),
                "radix sort");
-  if (!rc) {
+  const int groups = gather_groups_env();
+  if (!rc && groups > 1) {
+    rc = pbytes == 8 ? gather_grouped<double>(src, src_ids, dst, dst_ids, i_out, n, groups, s)
+                     : gather_grouped<float>(src, src_ids, dst, dst_ids, i_out, n, groups, s);
+  } else if (!rc) {
     if (pbytes == 8)
       gather_perm8<double><<<blocks_for(n), 256, 0, s>>>(
           (const double*)src[0], (const double*)src[1], (const double*)src[2],
