@@ -269,3 +269,26 @@ def test_inplace_and_swap_sorts_agree(gpu):
     with pytest.raises(DomainError):
         d3.sort_by_cell(geom)
     assert torch.equal(d3.ids, before)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 3, 5, 1027, 100_003])
+def test_device_sort_every_array_ragged(gpu, dtype, n):
+    """The grouped gather of the sort (three in-order passes, four
+    destinations per thread, a ragged tail) moves all eight arrays exactly as
+    the stable numpy permutation, for sizes that are not multiples of 4."""
+    import torch
+    from paper_2008_04397_b200.geometry import GridGeometry
+    from paper_2008_04397_b200.particles import DeviceParticles, ParticleBuffer
+    geom = GridGeometry.from_box((16, 8, 4), (3.2, 1.6, 0.8))
+    rng = np.random.default_rng(n)
+    b = ParticleBuffer.empty(n, dtype=dtype)
+    for a, L in zip("xyz", geom.lengths):
+        getattr(b, a)[:] = (rng.random(n) * L).astype(dtype)
+    for a in ("u", "v", "w", "q_p"):
+        getattr(b, a)[:] = rng.standard_normal(n).astype(dtype)
+    b.ids[:] = rng.permutation(n).astype(np.int64) * 7 + 3
+    order = np.argsort(geom.cell_index_of(b.x, b.y, b.z), kind="stable")
+    d = DeviceParticles.from_host(b, torch.device("cuda")).sort_by_cell(geom)
+    for a in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
+        assert np.array_equal(getattr(d, a).cpu().numpy(), getattr(b, a)[order]), a
