@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "bp_launch.h"
 
@@ -351,14 +352,60 @@ int cell_keys(int pbytes, const void* xs, const void* ys, const void* zs, int64_
   return hbad ? 3 : 0;
 }
 
-// Grow-only sort workspace per device (keys, indices, permutation scratch,
-// CUB temp storage), so periodic sorts do not re-allocate ~40 B/particle.
+// Grow-only sort workspaces (keys, indices, permutation scratch, CUB temp
+// storage), so periodic sorts do not re-allocate ~40 B/particle.  A sort
+// leases an idle workspace of its device for the whole call, so sorts of
+// different species on different streams (and host threads) run
+// concurrently; the pool grows to the number of concurrent sorts.
 struct SortWs {
   void* base = nullptr;
   size_t bytes = 0;
+  int dev = -1;
+  bool busy = false;
 };
 static std::mutex g_sort_mu;
-static SortWs g_sort_ws[64];
+static std::vector<SortWs*> g_sort_pool;
+
+class WsLease {
+ public:
+  // *rc = 0 and ws() >= need bytes on success
+  WsLease(size_t need, cudaStream_t s, int* rc) : s_(s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lock(g_sort_mu);
+      for (SortWs* w : g_sort_pool)
+        if (w->dev == dev && !w->busy && (!w_ || w->bytes > w_->bytes)) w_ = w;
+      if (!w_) {
+        w_ = new SortWs;
+        w_->dev = dev;
+        g_sort_pool.push_back(w_);
+      }
+      w_->busy = true;
+    }
+    *rc = 0;
+    if (w_->bytes < need) {
+      if (w_->base) {
+        cudaStreamSynchronize(s);
+        cudaFree(w_->base);  // also waits for the device's other streams
+        w_->base = nullptr;
+        w_->bytes = 0;
+      }
+      *rc = check(cudaMalloc(&w_->base, need), "sort workspace");
+      if (!*rc) w_->bytes = need;
+    }
+  }
+  ~WsLease() {
+    cudaStreamSynchronize(s_);  // (early error returns may leave work queued)
+    std::lock_guard<std::mutex> lock(g_sort_mu);
+    w_->busy = false;
+  }
+  void* base() const { return w_->base; }
+
+ private:
+  SortWs* w_ = nullptr;
+  cudaStream_t s_;
+};
 
 int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, void* ws,
                  void* qs, int64_t* ids, int64_t n, const double* origin,
@@ -377,22 +424,10 @@ int sort_by_cell(int pbytes, void* xs, void* ys, void* zs, void* us, void* vs, v
   auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
   const size_t nb = up((size_t)n * sizeof(uint32_t));
   const size_t need = 4 * nb + up(sizeof(int)) + up((size_t)n * 8) + up(cub_bytes);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(g_sort_mu);
-  SortWs& W = g_sort_ws[dev & 63];
-  if (W.bytes < need) {
-    if (W.base) {
-      cudaStreamSynchronize(s);
-      cudaFree(W.base);
-      W.base = nullptr;
-      W.bytes = 0;
-    }
-    int rc = check(cudaMalloc(&W.base, need), "sort workspace");
-    if (rc) return rc;
-    W.bytes = need;
-  }
-  char* p = static_cast<char*>(W.base);
+  int lrc = 0;
+  WsLease lease(need, s, &lrc);
+  if (lrc) return lrc;
+  char* p = static_cast<char*>(lease.base());
   uint32_t* k_in = (uint32_t*)p; p += nb;
   uint32_t* k_out = (uint32_t*)p; p += nb;
   uint32_t* i_in = (uint32_t*)p; p += nb;
@@ -442,22 +477,10 @@ int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* cons
   auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
   const size_t nb = up((size_t)n * sizeof(uint32_t));
   const size_t need = 4 * nb + up(sizeof(int)) + up((size_t)n * 8) + up(cub_bytes);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(g_sort_mu);
-  SortWs& W = g_sort_ws[dev & 63];
-  if (W.bytes < need) {
-    if (W.base) {
-      cudaStreamSynchronize(s);
-      cudaFree(W.base);
-      W.base = nullptr;
-      W.bytes = 0;
-    }
-    int rc = check(cudaMalloc(&W.base, need), "sort workspace");
-    if (rc) return rc;
-    W.bytes = need;
-  }
-  char* p = static_cast<char*>(W.base);
+  int lrc = 0;
+  WsLease lease(need, s, &lrc);
+  if (lrc) return lrc;
+  char* p = static_cast<char*>(lease.base());
   uint32_t* k_in = (uint32_t*)p; p += nb;
   uint32_t* k_out = (uint32_t*)p; p += nb;
   uint32_t* i_in = (uint32_t*)p; p += nb;
