@@ -292,3 +292,37 @@ def test_device_sort_every_array_ragged(gpu, dtype, n):
     d = DeviceParticles.from_host(b, torch.device("cuda")).sort_by_cell(geom)
     for a in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
         assert np.array_equal(getattr(d, a).cpu().numpy(), getattr(b, a)[order]), a
+
+
+def test_concurrent_sorts_on_side_streams(gpu):
+    """Sorts of different buffers from host threads on their own streams
+    (each leases its own workspace) give the sequential result."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2008_04397_b200.geometry import GridGeometry
+    from paper_2008_04397_b200.particles import DeviceParticles, ParticleBuffer
+    geom = GridGeometry.from_box((32, 16, 8), (6.4, 3.2, 1.6))
+    bufs = []
+    for k in range(4):
+        rng = np.random.default_rng(100 + k)
+        n = 400_000 + 13 * k
+        b = ParticleBuffer.empty(n, dtype=np.float32)
+        for a, L in zip("xyzuvw", geom.lengths + (1.0, 1.0, 1.0)):
+            getattr(b, a)[:] = (rng.random(n) * L).astype(np.float32)
+        bufs.append(b)
+    dev = torch.device("cuda")
+    seq = [DeviceParticles.from_host(b, dev).sort_by_cell(geom) for b in bufs]
+    par = [DeviceParticles.from_host(b, dev) for b in bufs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in par]
+
+    def one(i):
+        with torch.cuda.device(dev):
+            return par[i].sort_by_cell(geom, stream=streams[i])
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        list(ex.map(one, range(4)))
+    torch.cuda.synchronize()
+    for a, b in zip(seq, par):
+        for name in ("x", "y", "z", "u", "v", "w", "ids"):
+            assert torch.equal(getattr(a, name), getattr(b, name)), name
