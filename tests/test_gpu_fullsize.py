@@ -1,9 +1,9 @@
 """Full-size (C3) checks of the headline path: one species of the 3D GEM
-workload (128x64x64 cells, ppc 125: 65.5M electrons, f32) through the fast
-fused span on the device, against the oracle on every host core (the north
-star's 1e-4 relative to each array's max), plus the conservation identities
-the deposit satisfies at any size: sum over nodes of moment / invvol equals
-the particle sum of q, q v and q v v after the push."""
+workload (128x64x64 cells, ppc 125: 65.5M electrons, f32) against the oracle
+on every host core — bitwise in parity arithmetic; in fast arithmetic within
+the north star's 1e-4 relative to each array's max, plus the conservation
+identities the deposit satisfies at any size (sum over nodes of moment /
+invvol equals the particle sum of q, q v and q v v after the push)."""
 
 import os
 
@@ -92,3 +92,39 @@ def test_c3_species_fast_within_tolerance_and_conserving(gpu, oracle):
         # well inside 1e-5 of the sum of |contributions|
         scale = (q.abs() * mom[m].abs()).sum().item()
         assert abs(node[m] - part) <= 1e-5 * scale, (m, node[m], part, scale)
+
+
+def test_c3_species_parity_bitwise(gpu, oracle):
+    """The bitwise path at full size: 65.5M electrons through the parity
+    kernels equal the oracle (the reference arithmetic) bit for bit."""
+    import torch
+    from paper_2008_04397_b200 import kernels as K
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import (GemInit, gem_fields, gem_geometry, gem_species,
+                                           init_gem_device)
+    geom = gem_geometry((128, 64, 64))
+    species = gem_species(125)
+    prec = PrecisionMode.from_label("single")
+    dev = torch.device("cuda")
+    p = init_gem_device(geom, species, dev, precision=prec)[0]
+    n = p.n
+    f = gem_fields(geom, GemInit(), prec)
+    E = _smooth_e(geom, 1e-3).astype(np.float32)
+    B = np.ascontiguousarray(f.B, np.float32)
+    inv = geom.inv_node_volume(np.float32)
+    geo_f, geo_i = K.make_geo_arrays(geom, np.float32)
+    geo_g, _ = K.make_geo_arrays(geom, np.float32)
+    sc = K.kernel_scalars(species[0], 0.25, 1.0, np.float32)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"],
+            3, np.float32(SCALE), 0)
+    ref = [a.cpu().numpy() for a in p.arrays()]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    st_ref = oracle.fused_parallel(*ref, 0, n, E, B, acc_ref, inv, *tail, os.cpu_count() or 1)
+    d = list(p.arrays())
+    dE, dB, dinv = (torch.from_numpy(a).to(dev) for a in (E, B, inv))
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device=dev)
+    st = K.fused_span(*d, 0, n, dE, dB, dacc, dinv, *tail, arith="parity")
+    assert st == st_ref
+    for name, r, t in zip("xyzuvw", ref, d[:6]):
+        assert np.array_equal(r, t.cpu().numpy()), name
+    assert np.array_equal(acc_ref, dacc.cpu().numpy())
