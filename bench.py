@@ -75,12 +75,14 @@ def parse():
 def workload_config(args, world):
     cells = tuple(int(c) for c in args.cells.split(","))
     n = int(np.prod(cells)) * args.ppc * 4
+    dim = "2d" if cells[2] == 1 else "3d"
+    traffic = n * 13 * (8 if args.precision == "double" else 4) / 1e9
     return cells, n, {
-        "workload": f"gem3d_{cells[0]}x{cells[1]}x{cells[2]}_ppc{args.ppc}x4",
+        "workload": f"gem{dim}_{cells[0]}x{cells[1]}x{cells[2]}_ppc{args.ppc}x4",
         "cells": list(cells), "particles": n, "species": 4, "ppc": args.ppc,
         "precision": args.precision, "arith": args.arith, "mover_iters": 3, "dt": 0.25,
         "sort_period": args.sort_period, "decomposition": f"particles/{world} ranks",
-        "l2_flush": "none: 13.6 GB of particle traffic per step >> 126 MB L2",
+        "l2_flush": f"none: {traffic:.1f} GB of particle traffic per step >> 126 MB L2",
     }
 
 

@@ -53,7 +53,12 @@ def gem_species(ppc, mover_iters=3):
     )
 
 
-def gem_geometry(cells, lengths=(25.6, 12.8, 12.8)):
+def gem_geometry(cells, lengths=None):
+    """GEM box 25.6 x 12.8 x 12.8 (gem_full.deck); a 2D grid (one cell in z)
+    takes lz = dx as the reference's 2D decks do."""
+    if lengths is None:
+        lz = 25.6 / cells[0] if cells[2] == 1 else 12.8
+        lengths = (25.6, 12.8, lz)
     return GridGeometry.from_box(cells, lengths, bc=(PERIODIC, REFLECTING, PERIODIC))
 
 

@@ -128,3 +128,66 @@ def test_c3_species_parity_bitwise(gpu, oracle):
     for name, r, t in zip("xyzuvw", ref, d[:6]):
         assert np.array_equal(r, t.cpu().numpy()), name
     assert np.array_equal(acc_ref, dacc.cpu().numpy())
+
+
+def _species0(cells, label, amp):
+    """Sheet electrons of the GEM workload on `cells` in precision `label`,
+    a smooth E of amplitude `amp`, the kernel argument tail and host copies."""
+    import torch
+    from paper_2008_04397_b200 import kernels as K
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import (GemInit, gem_fields, gem_geometry, gem_species,
+                                           init_gem_device)
+    geom = gem_geometry(cells)
+    species = gem_species(125)
+    prec = PrecisionMode.from_label(label)
+    pd, fd = prec.particle_dtype, prec.field_dtype
+    p = init_gem_device(geom, species, torch.device("cuda"), precision=prec)[0]
+    f = gem_fields(geom, GemInit(), prec)
+    E = _smooth_e(geom, amp).astype(fd)
+    B = np.ascontiguousarray(f.B, fd)
+    inv = geom.inv_node_volume(fd)
+    geo_f, geo_i = K.make_geo_arrays(geom, pd)
+    geo_g, _ = K.make_geo_arrays(geom, fd)
+    sc = K.kernel_scalars(species[0], 0.25, 1.0, pd)
+    tail = (geo_f, geo_g, geo_i, sc["dt"], sc["dth"], sc["qdt2m"], sc["beta"], sc["one"],
+            3, fd(SCALE), 1 if pd != fd else 0)
+    return geom, p, E, B, inv, tail
+
+
+@pytest.mark.parametrize("arith", ["parity", "fast"])
+def test_c2_species_double(gpu, oracle, arith):
+    """C2 (2D GEM at paper scale, 256x128x1, ppc 125) in f64: 4.1M sheet
+    electrons bitwise (parity) or within 1e-10 (fast) of the oracle."""
+    import torch
+    from paper_2008_04397_b200 import kernels as K
+    geom, p, E, B, inv, tail = _species0((256, 128, 1), "double", 1e-3)
+    n = p.n
+    assert n == 256 * 128 * 125
+    ref = [a.cpu().numpy() for a in p.arrays()]
+    acc_ref = np.zeros((10,) + geom.node_shape, np.int64)
+    st_ref = oracle.fused_parallel(*ref, 0, n, E, B, acc_ref, inv, *tail, os.cpu_count() or 1)
+    d = list(p.arrays())
+    dE, dB, dinv = (torch.from_numpy(a).cuda() for a in (E, B, inv))
+    dacc = torch.zeros((10,) + geom.node_shape, dtype=torch.int64, device="cuda")
+    st = K.fused_span(*d, 0, n, dE, dB, dacc, dinv, *tail, arith=arith)
+    assert st == st_ref == 0
+    got = [t.cpu().numpy() for t in d[:6]]
+    if arith == "parity":
+        for name, r, t in zip("xyzuvw", ref, got):
+            assert np.array_equal(r, t), name
+        assert np.array_equal(acc_ref, dacc.cpu().numpy())
+        return
+    periods = (geom.Lx, None, geom.Lz, None, None, None)
+    for name, r, t, per in zip("xyzuvw", ref, got, periods):
+        _assert_close(name, r, t, 1e-10, per)
+    # the moments live on the 2^-43 lattice: a contribution within an ulp of a
+    # half quantum rounds either way, so next to 1e-10 of the array max a few
+    # quanta per node are the reference's own quantisation (on the small
+    # current rows one quantum is more than 1e-10 of the row's max)
+    acc = dacc.cpu().numpy()
+    for m in range(10):
+        diff = np.abs(acc[m] - acc_ref[m])
+        bound = 1e-10 * np.abs(acc_ref[m]).max() + 4
+        assert diff.max() <= bound, (m, int(diff.max()), bound)
+        assert (diff > 0).mean() < 1e-3, (m, float((diff > 0).mean()))
