@@ -664,10 +664,11 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
   const int comp[6] = {0, 1, 3, 4, 2, 5};  // component of pair slot 2p + member
   double e2max = 0.0;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += gridDim.x * blockDim.x) {
-    // threads walk the cells k fastest (coalesced field reads, k is the
-    // fastest index of E / B); records are stored x fastest (sort order)
-    const int k = t % nz, j = (t / nz) % ny, i = t / (nz * ny);
-    const int c = i + nx * (j + ny * k);
+    // threads walk the cells in record order (x fastest, the particles' sort
+    // order): a warp writes 32 consecutive 48-value records; the strided
+    // field reads hit L2 (E / B are a few MB)
+    const int c = t;
+    const int i = t % nx, j = (t / nx) % ny, k = t / (nx * ny);
     const int n0 = (i * NY + j) * NZ + k;
     const int sx = NY * NZ, sy = NZ;
     double co[6][8];
