@@ -656,30 +656,54 @@ __global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constan
 // component pairs (a, b) = (Ex, Ey), (Bx, By), (Ez, Bz), four quads each:
 // (c0a c0b c1a c1b) (c2a c2b c4a c4b) (c3a c3b c5a c5b) (c6a c6b c7a c7b);
 // after the records, max |E| over the nodes (float, rounded up).
+// Tiles of 32 (x) x 8 (z) cells at one y: the 33 x 2 x 9 nodes of the six
+// components are staged in shared memory with k-fastest (coalesced) reads,
+// then warp w builds the records of z-row k0 + w, one cell per lane, and
+// writes 32 consecutive records (x fastest, the particles' sort order).
+constexpr int kPackTI = 32, kPackTK = 8, kPackRow = 19;  // 2 x 9 node values + 1 pad
+
 template <typename F, typename O>
-__global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int nx, int ny,
-                           int nz, O* __restrict__ rec, unsigned* __restrict__ emax_bits) {
+__global__ void __launch_bounds__(256) pack_cells(const F* __restrict__ E,
+                                                  const F* __restrict__ B, int nx, int ny,
+                                                  int nz, O* __restrict__ rec,
+                                                  unsigned* __restrict__ emax_bits) {
+  __shared__ F nodes[6][kPackTI + 1][kPackRow];
+  __shared__ unsigned wmax[8];
+  // the warp's 32 records, written out as contiguous 512-byte rows
+  extern __shared__ __align__(16) unsigned char pack_out_raw[];
+  O* const wout = reinterpret_cast<O*>(pack_out_raw) + (threadIdx.x >> 5) * (kPackTI * 48);
   const int NY = ny + 1, NZ = nz + 1, NN = (nx + 1) * NY * NZ;
-  const int ncell = nx * ny * nz;
   const int comp[6] = {0, 1, 3, 4, 2, 5};  // component of pair slot 2p + member
+  const int tx = (nx + kPackTI - 1) / kPackTI;
+  const int i0 = (blockIdx.x % tx) * kPackTI, k0 = (blockIdx.x / tx) * kPackTK;
+  const int j = blockIdx.y;
+  // stage: (h, i', j', k') with k' fastest; nodes past the grid are not read
+  constexpr int kVals = 6 * (kPackTI + 1) * 18;
+  for (int v = threadIdx.x; v < kVals; v += blockDim.x) {
+    const int kk = v % 9, jj = (v / 9) & 1, ii = (v / 18) % (kPackTI + 1), h = v / (18 * (kPackTI + 1));
+    const int gi = i0 + ii, gk = k0 + kk;
+    F val = F(0);
+    if (gi <= nx && gk <= nz) {
+      const int m = comp[h];
+      const F* f = m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN;
+      val = f[((size_t)gi * NY + (j + jj)) * NZ + gk];
+    }
+    nodes[h][ii][jj * 9 + kk] = val;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = i0 + lane, k = k0 + w;
   double e2max = 0.0;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ncell; t += gridDim.x * blockDim.x) {
-    // threads walk the cells in record order (x fastest, the particles' sort
-    // order): a warp writes 32 consecutive 48-value records; the strided
-    // field reads hit L2 (E / B are a few MB)
-    const int c = t;
-    const int i = t % nx, j = (t / nx) % ny, k = t / (nx * ny);
-    const int n0 = (i * NY + j) * NZ + k;
-    const int sx = NY * NZ, sy = NZ;
+  if (i < nx && k < nz) {
     double co[6][8];
     double e2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int h = 0; h < 6; ++h) {
-      const int m = comp[h];
-      const F* f = (m < 3 ? E + (size_t)m * NN : B + (size_t)(m - 3) * NN) + n0;
-      const double f000 = f[0], f100 = f[sx], f010 = f[sy], f110 = f[sx + sy];
-      const double f001 = f[1], f101 = f[sx + 1], f011 = f[sy + 1], f111 = f[sx + sy + 1];
-      if (m < 3) {
+      const F* r0 = nodes[h][lane];
+      const F* r1 = nodes[h][lane + 1];
+      const double f000 = r0[w], f100 = r1[w], f010 = r0[9 + w], f110 = r1[9 + w];
+      const double f001 = r0[w + 1], f101 = r1[w + 1], f011 = r0[10 + w], f111 = r1[10 + w];
+      if (comp[h] < 3) {
         e2[0] += f000 * f000; e2[1] += f100 * f100; e2[2] += f010 * f010; e2[3] += f110 * f110;
         e2[4] += f001 * f001; e2[5] += f101 * f101; e2[6] += f011 * f011; e2[7] += f111 * f111;
       }
@@ -692,7 +716,7 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
       co[h][6] = (f011 - f001) - (f010 - f000);
       co[h][7] = ((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000));
     }
-    O* o = rec + (size_t)c * 48;
+    O* o = wout + lane * 48;
     const int slot[4][2] = {{0, 1}, {2, 4}, {3, 5}, {6, 7}};
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr)
@@ -707,11 +731,28 @@ __global__ void pack_cells(const F* __restrict__ E, const F* __restrict__ B, int
 #pragma unroll
     for (int q = 0; q < 8; ++q) e2max = fmax(e2max, e2[q]);
   }
-  // non-negative floats order like their bit patterns; rounded up
+  __syncwarp();
+  if (k < nz) {
+    // this warp's cells i0 .. i0 + n - 1 of row (j, k): n * 48 contiguous values
+    const int n = min(kPackTI, nx - i0);
+    O* dst = rec + ((size_t)i0 + (size_t)nx * (j + (size_t)ny * k)) * 48;
+    const float4* src4 = reinterpret_cast<const float4*>(wout);
+    float4* dst4 = reinterpret_cast<float4*>(dst);
+    const int n16 = n * 48 * (int)sizeof(O) / 16;
+    for (int v = lane; v < n16; v += 32) __stcs(dst4 + v, src4[v]);
+  }
+  // non-negative floats order like their bit patterns; rounded up; one
+  // atomic per block
   unsigned bits = __float_as_uint(__double2float_ru(sqrt(e2max)));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
-  if ((threadIdx.x & 31) == 0 && bits) atomicMax(emax_bits, bits);
+  for (int sh = 16; sh > 0; sh >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, sh));
+  if (lane == 0) wmax[w] = bits;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+    for (int q = 0; q < 8; ++q) m = max(m, wmax[q]);
+    if (m) atomicMax(emax_bits, m);
+  }
 }
 
 }  // namespace sk
@@ -891,26 +932,39 @@ size_t split_records_bytes(int pbytes, const int64_t* geo_i) {
 int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
                        const int64_t* geo_i, void* rec, cudaStream_t s) {
   const int nx = (int)geo_i[0], ny = (int)geo_i[1], nz = (int)geo_i[2];
-  const long long ncell = (long long)nx * ny * nz;
-  int blocks = (int)((ncell + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  const dim3 blocks((unsigned)(((nx + sk::kPackTI - 1) / sk::kPackTI) *
+                               ((nz + sk::kPackTK - 1) / sk::kPackTK)),
+                    (unsigned)ny);
   unsigned* emax =
       reinterpret_cast<unsigned*>((char*)rec + split_records_bytes(pbytes, geo_i) - 32);
   cudaMemsetAsync(emax, 0, 32, s);
   const int th = timing_begin(TK_RECORDS, s);
+  const size_t osm = (size_t)8 * sk::kPackTI * 48 * (pbytes == 8 ? 8 : 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sk::pack_cells<double, double>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 8);
+    cudaFuncSetAttribute(sk::pack_cells<float, double>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 8);
+    cudaFuncSetAttribute(sk::pack_cells<double, float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
+    cudaFuncSetAttribute(sk::pack_cells<float, float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
+    attr = true;
+  }
   if (pbytes == 8) {
     if (fbytes == 8)
-      sk::pack_cells<double, double><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B,
+      sk::pack_cells<double, double><<<blocks, 256, osm, s>>>((const double*)E, (const double*)B,
                                                             nx, ny, nz, (double*)rec, emax);
     else
-      sk::pack_cells<float, double><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B,
+      sk::pack_cells<float, double><<<blocks, 256, osm, s>>>((const float*)E, (const float*)B,
                                                            nx, ny, nz, (double*)rec, emax);
   } else {
     if (fbytes == 8)
-      sk::pack_cells<double, float><<<blocks, 256, 0, s>>>((const double*)E, (const double*)B,
+      sk::pack_cells<double, float><<<blocks, 256, osm, s>>>((const double*)E, (const double*)B,
                                                            nx, ny, nz, (float*)rec, emax);
     else
-      sk::pack_cells<float, float><<<blocks, 256, 0, s>>>((const float*)E, (const float*)B, nx,
+      sk::pack_cells<float, float><<<blocks, 256, osm, s>>>((const float*)E, (const float*)B, nx,
                                                           ny, nz, (float*)rec, emax);
   }
   timing_end(th, s);

@@ -429,3 +429,63 @@ def test_fast_split_tiny_spans(gpu, oracle, count):
     for m in range(10):
         if count:
             _assert_close(f"moment {m}", acc_ref[m] * 2.0 ** -43, got[m] * 2.0 ** -43, 1e-4)
+
+
+def _host_records(E, B, nx, ny, nz, out_dtype):
+    """The cell-record contract of bp_field_records_build on the host: per cell
+    (x fastest) the trilinear coefficients of (Ex Ey | Bx By | Ez Bz) from the
+    8 nodes in f64, rounded once; then max |E| over the nodes, rounded up."""
+    F = [np.asarray(E[0], np.float64), np.asarray(E[1], np.float64), np.asarray(E[2], np.float64),
+         np.asarray(B[0], np.float64), np.asarray(B[1], np.float64), np.asarray(B[2], np.float64)]
+    comp = (0, 1, 3, 4, 2, 5)
+    co = []
+    for m in comp:
+        f = F[m]
+        f000, f100, f010, f110 = f[:-1, :-1, :-1], f[1:, :-1, :-1], f[:-1, 1:, :-1], f[1:, 1:, :-1]
+        f001, f101, f011, f111 = f[:-1, :-1, 1:], f[1:, :-1, 1:], f[:-1, 1:, 1:], f[1:, 1:, 1:]
+        co.append([f000, f100 - f000, f010 - f000, f001 - f000,
+                   (f110 - f100) - (f010 - f000), (f101 - f001) - (f100 - f000),
+                   (f011 - f001) - (f010 - f000),
+                   ((f111 - f011) - (f101 - f001)) - ((f110 - f010) - (f100 - f000))])
+    slot = ((0, 1), (2, 4), (3, 5), (6, 7))
+    rec = np.empty((nz, ny, nx, 48), out_dtype)  # cell index i + nx (j + ny k)
+    q = 0
+    for pr in range(3):
+        for a, b in slot:
+            for v in (co[2 * pr][a], co[2 * pr + 1][a], co[2 * pr][b], co[2 * pr + 1][b]):
+                rec[..., q] = v.transpose(2, 1, 0).astype(out_dtype)
+                q += 1
+    e2 = F[0] ** 2 + F[1] ** 2 + F[2] ** 2
+    return rec.reshape(-1), np.sqrt(e2.max())
+
+
+@pytest.mark.parametrize("cells", [(13, 7, 5), (64, 3, 17), (33, 2, 1)])
+def test_cell_records_match_host_formula(gpu, cells):
+    """bp_field_records_build (tiles of 32 x 8 cells, partial tiles at the
+    grid edge included) writes exactly the host-computed records and an
+    upper bound on max |E| that is its f32 round-up."""
+    import ctypes
+    from paper_2008_04397_b200 import _lib
+    torch = gpu
+    L = _lib.load()
+    nx, ny, nz = cells
+    rng = np.random.default_rng(sum(cells))
+    E = rng.standard_normal((3, nx + 1, ny + 1, nz + 1)).astype(np.float32)
+    B = rng.standard_normal((3, nx + 1, ny + 1, nz + 1)).astype(np.float32)
+    gi = np.array([nx, ny, nz, 0, 1, 0], np.int64)
+    nbytes = L.bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data))
+    rec = torch.zeros(nbytes // 4 + 64, dtype=torch.float32, device="cuda")
+    ptr = (rec.data_ptr() + 255) & ~255
+    off = (ptr - rec.data_ptr()) // 4
+    dE, dB = _dev(torch, [E, B])
+    assert L.bp_field_records_build(4, 4, ctypes.c_void_p(dE.data_ptr()),
+                                    ctypes.c_void_p(dB.data_ptr()),
+                                    ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    torch.cuda.synchronize()
+    got = rec.cpu().numpy()[off:off + nbytes // 4]
+    want, emax = _host_records(E, B, nx, ny, nz, np.float32)
+    assert np.array_equal(got[:want.size], want)
+    g_emax = got[want.size]
+    assert g_emax >= emax and g_emax == np.float32(np.nextafter(np.float32(emax), np.inf)) or \
+        g_emax == np.float32(emax)
