@@ -597,11 +597,21 @@ int bp_sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* c
     set_error("src and dst arrays are required");
     return BP_EINVAL;
   }
-  for (int k = 0; k < 6; ++k)
-    if (!src[k] || !dst[k] || src[k] == dst[k]) {
+  for (int k = 0; k < 7; ++k) {
+    // x..w are required, q (k = 6) is optional but must then be given on both sides
+    if (k < 6 && (!src[k] || !dst[k])) {
+      set_error("sort_by_cell_into needs x, y, z, u, v, w on both sides");
+      return BP_EINVAL;
+    }
+    if ((src[k] == nullptr) != (dst[k] == nullptr) || (src[k] && src[k] == dst[k])) {
       set_error("sort_by_cell_into needs distinct source and destination arrays");
       return BP_EINVAL;
     }
+  }
+  if ((src_ids == nullptr) != (dst_ids == nullptr) || (src_ids && src_ids == dst_ids)) {
+    set_error("sort_by_cell_into needs distinct source and destination id arrays");
+    return BP_EINVAL;
+  }
   ensure_pool();
   return sort_by_cell_into(pbytes, src, src_ids, dst, dst_ids, n, origin, spacing, counts,
                            (cudaStream_t)stream);

@@ -55,4 +55,15 @@ void timing_end(int handle, cudaStream_t s);
 // keep the default stream-ordered pool's memory mapped between calls
 void ensure_pool();
 
+// True the first time it is called for the current device with this flag
+// array (kernel attributes such as the dynamic shared memory limit are per
+// device, so a process driving two GPUs must set them on each).
+inline bool first_on_device(bool (&flags)[64]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  if (flags[dev]) return false;
+  flags[dev] = true;
+  return true;
+}
+
 }  // namespace bp

@@ -128,11 +128,9 @@ int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t c
   constexpr size_t kStageOnly = (size_t)(kThreads / 32) * kWarpStage * sizeof(double);
   // a push-only launch without TMA tiles touches no shared memory
   const size_t smem = a.bulk ? kFull : (DEP ? kStageOnly : 0);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFull);
-    attr = true;
-  }
   // one wave of resident blocks; every warp walks a contiguous run of >= 32
   const int grid = grid_for(k, smem, count, kThreads);
   const int th = timing_begin(TK_SPAN, s);

@@ -490,7 +490,14 @@ int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* cons
   void* cub_tmp = p;
   cudaMemsetAsync(bad, 0, sizeof(int), s);
   int rc = 0;
-  const int64_t n4 = pbytes == 4 ? n / 4 * 4 : 0;
+  // the vector kernels need 16-byte-aligned arrays (a shard view such as
+  // x[start:] may not be); otherwise the scalar kernels run
+  auto a16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vkeys = pbytes == 4 && a16(src[0]) && a16(src[1]) && a16(src[2]);
+  bool vgather = !dst_ids || a16(dst_ids);
+  for (int a = 0; a < 7; ++a)
+    if (dst[a] && !a16(dst[a])) vgather = false;
+  const int64_t n4 = vkeys ? n / 4 * 4 : 0;
   if (n4) {
     cell_key4_kernel<<<blocks_for(n4 / 4), 256, 0, s>>>(
         (const float*)src[0], (const float*)src[1], (const float*)src[2], n4, origin[0],
@@ -510,7 +517,25 @@ int sort_by_cell_into(int pbytes, void* const* src, int64_t* src_ids, void* cons
                                                0, end_bit, s),
                "radix sort");
   const int groups = gather_groups_env();
-  if (!rc && groups > 1) {
+  if (!rc && !vgather) {
+    for (int a = 0; a < 7 && !rc; ++a) {
+      if (!src[a]) continue;
+      if (pbytes == 8)
+        gather_perm<double><<<blocks_for(n), 256, 0, s>>>((const double*)src[a], i_out,
+                                                          (double*)dst[a], n);
+      else
+        gather_perm<float><<<blocks_for(n), 256, 0, s>>>((const float*)src[a], i_out,
+                                                         (float*)dst[a], n);
+      note_launch();
+      rc = check(cudaGetLastError(), "gather_perm");
+    }
+    if (!rc && src_ids) {
+      gather_perm<long long><<<blocks_for(n), 256, 0, s>>>((const long long*)src_ids, i_out,
+                                                           (long long*)dst_ids, n);
+      note_launch();
+      rc = check(cudaGetLastError(), "gather_perm");
+    }
+  } else if (!rc && groups > 1) {
     rc = pbytes == 8 ? gather_grouped<double>(src, src_ids, dst, dst_ids, i_out, n, groups, s)
                      : gather_grouped<float>(src, src_ids, dst, dst_ids, i_out, n, groups, s);
   } else if (!rc) {

@@ -824,11 +824,9 @@ int launch_deposit_cfg(const sk::Params<T>& a, cudaStream_t s) {
   auto k = sk::deposit_kernel<T, PX, CHUNK, MINB>;
   const size_t smem =
       (size_t)(256 / 32) * (sk::stage_len<T>() + sk::Patch<PX>::kLen) * sizeof(T);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
   const int g = grid_of(k, smem, (long long)CHUNK * 8, a.count);
   const int th = timing_begin(TK_DEPOSIT, s);
   k<<<g, 256, smem, s>>>(a);
@@ -940,8 +938,8 @@ int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
   cudaMemsetAsync(emax, 0, 32, s);
   const int th = timing_begin(TK_RECORDS, s);
   const size_t osm = (size_t)8 * sk::kPackTI * 48 * (pbytes == 8 ? 8 : 4);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(sk::pack_cells<double, double>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 8);
     cudaFuncSetAttribute(sk::pack_cells<float, double>,
@@ -950,7 +948,6 @@ int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
     cudaFuncSetAttribute(sk::pack_cells<float, float>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
-    attr = true;
   }
   if (pbytes == 8) {
     if (fbytes == 8)

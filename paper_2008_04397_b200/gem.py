@@ -101,6 +101,18 @@ def gem_fields(geom, init, precision=None):
     return f
 
 
+def smooth_e_field(geom, amp, dtype=np.float64):
+    """A smooth, periodic, non-zero E of amplitude ``amp`` on the nodes (the
+    GEM start has E = 0; benchmarks and tests use this so the E gather and
+    the boundary-skip test see a real field)."""
+    X, Y, Z = np.meshgrid(geom.node_coords(0), geom.node_coords(1), geom.node_coords(2),
+                          indexing="ij")
+    kx, ky, kz = (2 * np.pi / L for L in geom.lengths)
+    return (amp * np.stack([np.sin(kx * X + 0.3) * np.cos(ky * Y),
+                            np.cos(kz * Z) * np.sin(kx * X),
+                            np.sin(ky * Y + 0.7) * np.cos(kz * Z - 0.2)])).astype(dtype)
+
+
 def init_gem_host(geom, species, init=GemInit(), precision=None, c=1.0):
     """Bit-identical restatement of the reference loader (gem.py:64-115)."""
     _check(species)

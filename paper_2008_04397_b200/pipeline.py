@@ -41,13 +41,20 @@ def shard_span(n, rank, world):
     return partition_batches(n, world).spans[rank]
 
 
-def reduce_moments(accs, group=None, async_op=False):
-    """Exact all-reduce (int64 SUM) of per-species moment grids across the
-    ranks of ``group`` (NCCL for CUDA tensors, gloo for CPU tensors).  Returns
-    the work handles when ``async_op``."""
+def reduce_moments(accs, group=None, async_op=False, root=None):
+    """Exact int64 SUM of per-species moment grids across the ranks of
+    ``group`` (NCCL for CUDA tensors, gloo for CPU tensors): an all-reduce, or
+    with ``root`` a reduce onto that rank only (the host field solve runs on
+    one rank; the other ranks' grids are then unspecified).  Returns the work
+    handles when ``async_op``."""
     import torch.distributed as dist
-    works = [dist.all_reduce(a, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
-             for a in accs]
+    if root is None:
+        works = [dist.all_reduce(a, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+                 for a in accs]
+    else:
+        dst = root if group is None else dist.get_global_rank(group, root)
+        works = [dist.reduce(a, dst, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+                 for a in accs]
     return works if async_op else None
 
 
@@ -86,6 +93,9 @@ class DeviceSimulation:
     device: object = None
     group: object = None          # torch.distributed process group (None = default)
     distributed: bool = False
+    # "all": every rank ends the cycle with the summed moments (all-reduce);
+    # "root": only rank 0 (where the host solve runs) gets them (reduce)
+    reduce: str = "all"
 
     def __post_init__(self):
         import torch
@@ -123,6 +133,8 @@ class DeviceSimulation:
             gi = np.ascontiguousarray(self.geo_i, np.int64)
             nbytes = int(_lib.load().bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data)))
             self.records = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=self.device)
+        if self.reduce not in ("all", "root"):
+            raise ConfigurationError(f"reduce must be 'all' or 'root', not {self.reduce!r}")
         if self.distributed:
             import torch.distributed as dist
             self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
@@ -240,6 +252,9 @@ class DeviceSimulation:
             a.zero_()
         ev[1].record(s)
         works = []
+        # the cell records are built on `s` before any side stream forks off
+        # it (side streams wait on everything queued on `s` so far)
+        self._records_ptr(s)
         side = self._side_streams(s)
         for sid, p in enumerate(self.particles):
             if p is None or p.n == 0:
@@ -251,7 +266,8 @@ class DeviceSimulation:
             if reduce and self.distributed:
                 if side:
                     s.wait_stream(ss)
-                works += reduce_moments([self.acc[sid]], self.group, async_op=True)
+                works += reduce_moments([self.acc[sid]], self.group, async_op=True,
+                                        root=0 if self.reduce == "root" else None)
         for ss in side:
             s.wait_stream(ss)
         ev[2].record(s)

@@ -46,7 +46,7 @@ def _oracle_moments(O, geom, species, bufs, fields, spans):
     return out
 
 
-def _worker(rank, world, port, result):
+def _worker(rank, world, port, result, root=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -62,7 +62,7 @@ def _worker(rank, world, port, result):
         spans = [shard_span(b.n, rank, world) for b in bufs]
         accs = _oracle_moments(O, geom, species, bufs, fields, spans)
         t = [torch.from_numpy(a) for a in accs]
-        works = reduce_moments(t, async_op=True)
+        works = reduce_moments(t, async_op=True, root=root)
         for w in works:
             w.wait()
         if rank == 0:
@@ -84,7 +84,8 @@ def test_shards_cover_every_particle_once():
             assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
 
 
-def test_two_rank_reduce_equals_single_process():
+@pytest.mark.parametrize("root", [None, 0], ids=["allreduce", "reduce_to_root"])
+def test_two_rank_reduce_equals_single_process(root):
     from oracle import oracle as O
     O.build()
     geom, species, bufs, fields = _setup()
@@ -93,7 +94,7 @@ def test_two_rank_reduce_equals_single_process():
     port = _free_port()
     with mp.Manager() as m:
         result = m.dict()
-        mp.spawn(_worker, args=(2, port, result), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, port, result, root), nprocs=2, join=True)
         accs = result["accs"]
     for a, r in zip(accs, ref):
         assert np.array_equal(a, r)
