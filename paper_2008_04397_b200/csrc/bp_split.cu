@@ -31,44 +31,11 @@
 #include <type_traits>
 
 #include "bp_common.cuh"
+#include "bp_f32_common.cuh"
 #include "bp_launch.h"
 
 namespace bp {
 namespace sk {
-
-template <typename T>
-struct Params {
-  T *x, *y, *z, *u, *v, *w;
-  const T* q;
-  long long start, count;
-  const void* rec;     // 12 quads of T per cell, cell = i + nx * (j + ny * k)
-  const float* iv_f;   // invvol (nx+1, ny+1, nz+1) when fields are f32
-  const double* iv_d;  // ... when fields are f64
-  long long* acc;      // (10, NN) int64
-  int nx, ny, nz, NY, NZ, NN;
-  int cny;  // nx * ny (cell-record z stride)
-  T o[3], hi[3], L[3], hi2[3], idx[3], ogs[3];
-  T dt, dth, qdt2m, beta, beta2;
-  double scale;
-  int n_iters;
-  int* status;
-  unsigned long long* work;  // deposit: next unclaimed particle of the span
-  unsigned* skip;            // one bit per span particle the mover did not store
-  const float* emax;         // max |E| over the nodes (after the cell records)
-  T bc_eps[3];               // rounding slack of the boundary-skip test per axis
-};
-
-// record quad of T
-template <typename T>
-struct Quad;
-template <>
-struct Quad<float> {
-  typedef float4 type;
-};
-template <>
-struct Quad<double> {
-  typedef double4 type;
-};
 
 // staged row stride (elements): rows read by one warp LDS.128 land in
 // distinct banks (36 floats / 34 doubles = 4 mod 32 words)
@@ -80,117 +47,6 @@ __host__ __device__ constexpr int row_len() {
 template <typename T>
 __host__ __device__ constexpr int stage_len() {
   return 18 * row_len<T>();
-}
-
-__device__ __forceinline__ float rcp_fast(float d) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));  // d >= 1: MUFU.RCP alone
-  return r;
-}
-__device__ __forceinline__ double rcp_fast(double d) { return __drcp_rn(d); }
-
-// record loads (kept in L1 / L2 in preference to the particle streams)
-__device__ __forceinline__ void ldg_pair(const float4* p, float4& a, float4& b) {
-  asm("ld.global.nc.L1::evict_last.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-      : "l"(p));
-}
-__device__ __forceinline__ void ldg_pair(const double4* p, double4& a, double4& b) {
-  asm("ld.global.nc.L1::evict_last.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
-      : "=d"(a.x), "=d"(a.y), "=d"(a.z), "=d"(a.w)
-      : "l"(p));
-  asm("ld.global.nc.L1::evict_last.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
-      : "=d"(b.x), "=d"(b.y), "=d"(b.z), "=d"(b.w)
-      : "l"(p + 1));
-}
-
-template <bool REFL, typename T>
-__device__ __forceinline__ T fold_mid(T xm, T o, T L, T hi, T hi2) {
-  if (!REFL) {
-    if (xm < o) xm += L;
-    else if (xm > hi) xm -= L;
-  } else {
-    if (xm < o) xm = o + (o - xm);
-    else if (xm > hi) xm = hi2 - xm;
-  }
-  return xm;
-}
-
-template <bool REFL, typename T>
-__device__ __forceinline__ void fold_commit(T& q, T& vel, T o, T L, T hi, T hi2) {
-  if (!REFL) {
-    if (q < o) {
-      q += L;
-      if (q >= hi) q = o;
-    } else if (q >= hi) {
-      q -= L;
-    }
-  } else {
-    if (q < o) {
-      q = o + (o - q);
-      vel = -vel;
-    } else if (q > hi) {
-      q = hi2 - q;
-      vel = -vel;
-    }
-  }
-}
-
-// True when no position of the push can leave the box: the implicit
-// rotation never lengthens t = v + qdt2m E (|v_bar| <= |t|),
-// and |E| at any point is at most its node maximum, so every midpoint and the
-// committed position lie within dt * (|v|_1 + |qdt2m| max|E|) of the start.
-template <typename T>
-__device__ __forceinline__ bool interior(const Params<T>& a, T qe, T x, T y, T z, T u, T v,
-                                         T w) {
-  const T reach = (fabs(u) + fabs(v) + fabs(w) + qe) * a.dt;
-  return x - a.o[0] > reach + a.bc_eps[0] && a.hi[0] - x > reach + a.bc_eps[0] &&
-         y - a.o[1] > reach + a.bc_eps[1] && a.hi[1] - y > reach + a.bc_eps[1] &&
-         z - a.o[2] > reach + a.bc_eps[2] && a.hi[2] - z > reach + a.bc_eps[2];
-}
-
-// cell of an in-box position: truncation (in-box gx >= -ulp truncates to 0)
-// and the upper-face clamp of kernels.py:541-556; returns the cell index
-template <typename T>
-__device__ __forceinline__ int cell_of(const Params<T>& a, T x, T y, T z, T& fx, T& fy, T& fz,
-                                       int& i, int& j, int& k) {
-  const T gx = fma(x, a.idx[0], -a.ogs[0]);
-  const T gy = fma(y, a.idx[1], -a.ogs[1]);
-  const T gz = fma(z, a.idx[2], -a.ogs[2]);
-  i = min((int)gx, a.nx - 1);
-  j = min((int)gy, a.ny - 1);
-  k = min((int)gz, a.nz - 1);
-  fx = gx - (T)i;
-  fy = gy - (T)j;
-  fz = gz - (T)k;
-  return i + a.nx * j + a.cny * k;
-}
-
-typedef float2 F2;
-__device__ __forceinline__ F2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
-
-// one component pair (a, b) from its four quads: A = c0a c0b c1a c1b,
-// B = c2a c2b c4a c4b, C = c3a c3b c5a c5b, D = c6a c6b c7a c7b
-__device__ __forceinline__ void tri_pair(const float4& A, const float4& B, const float4& C,
-                                         const float4& D, float fx, float fy, float fz,
-                                         float& ra, float& rb) {
-  const F2 FX = f2(fx, fx), FY = f2(fy, fy), FZ = f2(fz, fz);
-  const F2 p = fma2(f2(A.z, A.w), FX, f2(A.x, A.y));
-  const F2 q = fma2(f2(B.z, B.w), FX, f2(B.x, B.y));
-  const F2 r = fma2(f2(C.z, C.w), FX, f2(C.x, C.y));
-  const F2 t = fma2(f2(D.z, D.w), FX, f2(D.x, D.y));
-  const F2 o = fma2(fma2(t, FY, r), FZ, fma2(q, FY, p));
-  ra = o.x;
-  rb = o.y;
-}
-__device__ __forceinline__ void tri_pair(const double4& A, const double4& B, const double4& C,
-                                         const double4& D, double fx, double fy, double fz,
-                                         double& ra, double& rb) {
-  ra = fma(fma(fma(D.z, fx, D.x), fy, fma(C.z, fx, C.x)), fz,
-           fma(fma(B.z, fx, B.x), fy, fma(A.z, fx, A.x)));
-  rb = fma(fma(fma(D.w, fx, D.y), fy, fma(C.w, fx, C.y)), fz,
-           fma(fma(B.w, fx, B.y), fy, fma(A.w, fx, A.y)));
 }
 
 // skipbc (warp-uniform): the caller has shown that no position of this push
