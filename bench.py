@@ -8,8 +8,9 @@ Workload (BASELINE.json configs[2], the metric's "GEM 3D"): 128x64x64 cells,
 ("single" precision), dt 0.25, 3 mover iterations, decks/gem_full.deck
 physics; synthetic GEM-shaped particles drawn in HBM (gem.init_gem_device),
 the Harris + perturbation B of gem.py and a smooth non-zero E of amplitude
-1e-3 (gem.smooth_e_field; the GEM start has E = 0, which would flatter the
-mover's boundary-skip test).  The total population is
+1e-4 (gem.smooth_e_field: ten times the reconnection field 0.1 B0 vA ~ 1e-5
+of this deck; the GEM start has E = 0, which would flatter the mover's
+boundary-skip test).  The total population is
 fixed and split over the ranks by contiguous cell ranges (strong scaling).
 
 A step is one cycle of the device path: E/B broadcast (N>1), zeroing of the
@@ -53,7 +54,7 @@ BYTES_PER_PARTICLE = {"single": 52, "mixed": 52, "double": 104}  # 13 words, SUR
 # (bp_split.cu): the mover reads and writes x y z u v w, the deposit reads
 # x y z u v w q
 KERNEL_WORDS = {"mover": 12, "deposit": 7, "span": 13}
-E_AMP = 1e-3  # smooth E in the timed steps (gem.smooth_e_field)
+E_AMP = 1e-4  # smooth E in the timed steps (gem.smooth_e_field)
 
 
 def parse():

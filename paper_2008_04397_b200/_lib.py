@@ -30,6 +30,8 @@ EXPORTS = (
     "bp_fold_periodic_i64", "bp_moments_total", "bp_susceptibility",
     "bp_field_records_bytes", "bp_field_records_build", "bp_fused_span_rec",
     "bp_timing_enable", "bp_timing_read",
+    "bp_bins_leaver_bytes", "bp_bins_plan", "bp_bins_fill", "bp_bins_cycle", "bp_bins_export",
+    "bp_bins_reslack",
 )
 
 _P = ctypes.c_void_p
@@ -68,6 +70,15 @@ _SIGS = {
     "bp_fold_periodic_i64": (_INT, [_P, _I64, _P, _P]),
     "bp_moments_total": (_INT, [_P, _INT, _I64, _P, _P]),
     "bp_susceptibility": (_INT, [_P, _P, _INT, _INT, _D, _D, _I64, _P, _P]),
+    "bp_bins_leaver_bytes": (_INT, []),
+    "bp_bins_plan": (_INT, [_INT, _P, _P, _P, _I64, _P, _P, _P, _D, _INT, _P, _P, _P, _P]),
+    "bp_bins_fill": (_INT, [_INT] + [_P] * 8 + [_I64, _P, _P, _P, _P, _P, _P, _P]),
+    "bp_bins_cycle": (_INT, [_INT] + [_P] * 10 + [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,
+                                                   _P, _P]
+                      + [_P, _P, _P] + [_D] * 5 + [_INT, _D, _P, _P]),
+    "bp_bins_export": (_INT, [_P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
+    "bp_bins_reslack": (_INT, [_P, _P, _P, _P, _I64, _P, _I64, _P, _D, _INT, _P, _P, _P, _P, _P,
+                               _P]),
 }
 
 _lib = None

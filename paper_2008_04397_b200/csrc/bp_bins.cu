@@ -1,0 +1,1198 @@
+// Cell-binned fast path for f32 particles (DeviceSimulation layout "bins").
+//
+// The reference keeps every species as one flat SoA and restores cell order
+// with a stable sort every sort_period cycles (particles.py:157-167,
+// pipeline.py:300-304); between sorts the particles drift out of order, and
+// on a GPU every out-of-order particle costs the mover a field-record fetch
+// and the deposit a cross-lane regrouping.  Here a species lives in per-cell
+// bins instead: cell c owns slots [start[c], start[c + 1]) of the SoA arrays
+// (x y z u v w q + int64 ids, the reference's ParticleBuffer columns), the
+// first count[c] of them live.  Every cycle, per species:
+//
+//   mover_bins    one warp per bin: the bin's cell record (bp_split.cu's
+//                 trilinear coefficient form) is loaded ONCE into registers
+//                 and serves every midpoint gather inside the cell; the push
+//                 is the reference's (kernels.py:498-676) in native f32.
+//                 Particles whose new cell differs ("leavers") are written
+//                 to a leaver list and their slots are refilled from the
+//                 bin's tail, so a bin stays dense.
+//   migrate_bins  every leaver is appended to its new cell's bin.
+//   deposit_bins  a quarter-warp (8 lanes) per bin: all of a bin's particles
+//                 share one cell, so each lane accumulates the 80 products
+//                 (10 moments x 8 corners, kernels.py:689-734) of its
+//                 particles in registers with FFMA2; one shared-memory
+//                 transpose per bin reduces the 8 lanes, and each lane adds
+//                 one corner's 10 sums onto the int64 lattice (x invvol x
+//                 2^43, rint; fields.py:20-25) with REDG.ADD.64.
+//
+// So the particles are cell-sorted at every cycle, not every tenth, and
+// neither kernel does per-particle regrouping.  Bins have slack (the build
+// sizes them count + max(min, frac x count)); a leaver that finds its bin
+// full goes to an overflow list, deposited on its own, and the host rebuilds
+// the species' bins at the end of the cycle.  Particles that could not be
+// listed as leavers stay in their old bin ("misplaced"): both kernels test
+// each particle's cell and handle those on a slow path, and the host
+// rebuilds too.  Arithmetic: as bp_split.cu (fast f32, within the north
+// star's 1e-4 of the reference); the f32 per-bin sums are rounded once onto
+// the lattice.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "bp_f32_common.cuh"
+#include "bp_launch.h"
+
+namespace bp {
+namespace bins {
+
+using sk::F2;
+using sk::f2;
+using sk::fma2;
+typedef sk::Params<float> P;
+
+// a leaver in transit: 48 bytes
+struct __align__(16) Leaver {
+  float4 a;  // x y z u
+  float4 b;  // v w q, destination cell (int bits; < 0: no particle)
+  long long id;
+  long long pad;
+};
+
+enum {
+  ST_LEAVERS = 0,    // leaver slots claimed this cycle
+  ST_OVERFLOW = 1,   // leavers that found their bin full
+  ST_MISPLACED = 2,  // particles left in a bin that is not their cell
+  ST_LOST = 3,       // overflow list full: particles dropped (fatal)
+  ST_WORK_MOVE = 4,  // work counters
+  ST_WORK_DEP = 5,
+  ST_LATE = 6,       // misplaced particles the deposit listed for deposit_list
+  ST_N = 8
+};
+
+struct Bins {
+  float *x, *y, *z, *u, *v, *w, *q;
+  long long* id;
+  const long long* start;  // [ncell + 1]
+  int* count;              // [ncell]
+  int ncell;
+  Leaver* lv;
+  long long lv_cap;
+  Leaver* ov;
+  long long ov_cap;
+  Leaver* late;  // the deposit's misplaced particles (deposited by deposit_list)
+  long long late_cap;
+  unsigned long long* stat;  // [ST_N]
+  int variant;  // measurement knobs (BP_BINS_VARIANT), 0 = default
+};
+
+// particle stream loads / stores by variant: 0 streaming (.cs), 1 read-only
+// path (.nc), 2 default caching
+__device__ __forceinline__ float ld_p(const float* p, int v) {
+  return v == 0 ? __ldcs(p) : (v == 1 ? __ldg(p) : *p);
+}
+__device__ __forceinline__ void st_p(float* p, float x, int v) {
+  if (v == 0) __stcs(p, x);
+  else *p = x;
+}
+
+constexpr int kHoleCap = 64;     // leavers per bin per cycle tracked for the refill
+constexpr int kMoveClaim = 8;    // bins per mover work claim
+constexpr int kLvChunk = 128;    // leaver slots per warp reservation
+constexpr int kDepClaim = 16;    // bins per deposit work claim (4 rounds of 4)
+constexpr int kRowS = 84;        // deposit transpose row stride (floats)
+constexpr int kWarpSm = 32 * kRowS + 32;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Grid-unit box of cell (i, j, k): cell_of (bp_f32_common.cuh) puts gx in
+// cell i iff min(trunc(gx), n - 1) == i, i.e. gx in [lo, hi) with lo = i (the
+// largest float above -1 for i = 0: trunc maps (-1, 1) to 0) and hi = i + 1
+// (+inf for the last cell); fx = gx - i exactly as cell_of.
+struct Box {
+  float lo[3], hi[3], cf[3];
+};
+struct Ijk {
+  int i, j, k;
+};
+__device__ __forceinline__ Ijk ijk_of(const P& a, int c) {
+  return Ijk{c % a.nx, (c / a.nx) % a.ny, c / a.cny};
+}
+// the cell t positions further in x-fastest order
+__device__ __forceinline__ Ijk ijk_advance(const P& a, Ijk q, int t) {
+  q.i += t;
+  while (q.i >= a.nx) {
+    q.i -= a.nx;
+    if (++q.j == a.ny) {
+      q.j = 0;
+      ++q.k;
+    }
+  }
+  return q;
+}
+__device__ __forceinline__ Box cell_box(const P& a, Ijk q) {
+  Box b;
+  const int idx[3] = {q.i, q.j, q.k};
+  const int n[3] = {a.nx, a.ny, a.nz};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    b.cf[d] = (float)idx[d];
+    b.lo[d] = idx[d] == 0 ? __int_as_float(0xbf7fffff) : b.cf[d];
+    b.hi[d] = idx[d] == n[d] - 1 ? __int_as_float(0x7f800000) : b.cf[d] + 1.f;
+  }
+  return b;
+}
+
+__device__ __forceinline__ bool in_box(const Box& b, float gx, float gy, float gz) {
+  return gx >= b.lo[0] && gx < b.hi[0] && gy >= b.lo[1] && gy < b.hi[1] && gz >= b.lo[2] &&
+         gz < b.hi[2];
+}
+
+__device__ __forceinline__ void load_record(const P& a, int cell, float4 (&R)[12]) {
+  const float4* r = static_cast<const float4*>(a.rec) + (size_t)cell * 12;
+#pragma unroll
+  for (int q = 0; q < 12; q += 2) sk::ldg_pair(r + q, R[q], R[q + 1]);
+}
+
+// The implicit push (bp_split.cu push(), kernels.py:498-676 in native f32)
+// with the lane's record R of cell `held` kept across particles: a bin's
+// particles start in the bin's cell, so R (the bin's record, staged in shared
+// memory) serves nearly every midpoint, and only a lane whose midpoint lies
+// in another cell reloads it.  Every lane of the warp runs the whole push
+// (no early return: a failing particle keeps a safe position and reports
+// its status), so the reload is a warp-uniform branch.
+template <bool RX, bool RY, bool RZ>
+__device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, int home,
+                                        const float4* home_rec, float& xp, float& yp,
+                                        float& zp, float& un, float& vn, float& wn,
+                                        bool skipbc) {
+  float vbx = un, vby = vn, vbz = wn;
+  int st = ST_OK;
+#pragma unroll 1
+  for (int it = 0; it < a.n_iters; ++it) {
+    const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
+    float xm = XM.x, ym = XM.y;
+    float zm = fmaf(vbz, a.dth, zp);
+    if (!skipbc) {
+      xm = sk::fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+      ym = sk::fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+      zm = sk::fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+      if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
+          zm > a.hi[2]) {
+        st = ST_MIDPOINT;  // (kernels.py:535-538) carried on at a safe position
+        xm = xp; ym = yp; zm = zp;
+      }
+    }
+    float fx, fy, fz;
+    int i, j, k;
+    const int cell = sk::cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    const bool need = cell != held;
+    if (__any_sync(0xffffffffu, need)) {
+      if (need) {
+        held = cell;
+        if (cell == home) {  // back in the bin's cell: its record is in shared memory
+#pragma unroll
+          for (int q = 0; q < 12; ++q) R[q] = home_rec[q];
+        } else {
+          load_record(a, cell, R);
+        }
+      }
+    }
+    float ex, ey, hx, hy, ez, hz;
+    sk::tri_pair(R[0], R[1], R[2], R[3], fx, fy, fz, ex, ey);
+    sk::tri_pair(R[4], R[5], R[6], R[7], fx, fy, fz, hx, hy);
+    sk::tri_pair(R[8], R[9], R[10], R[11], fx, fy, fz, ez, hz);
+    const F2 Txy = fma2(f2(a.qdt2m, a.qdt2m), f2(ex, ey), f2(un, vn));
+    const float tx = Txy.x, ty = Txy.y;
+    const float tz = fmaf(a.qdt2m, ez, wn);
+    const float bsq = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+    const float inv = sk::rcp_fast(fmaf(a.beta2, bsq, 1.f));
+    const float tdb = fmaf(tx, hx, fmaf(ty, hy, tz * hz));
+    const float bt = a.beta * tdb;
+    const float cx = fmaf(ty, hz, -tz * hy), cy = fmaf(tz, hx, -tx * hz),
+                cz = fmaf(tx, hy, -ty * hx);
+    vbx = fmaf(a.beta, fmaf(bt, hx, cx), tx) * inv;
+    vby = fmaf(a.beta, fmaf(bt, hy, cy), ty) * inv;
+    vbz = fmaf(a.beta, fmaf(bt, hz, cz), tz) * inv;
+  }
+  if (st != ST_OK) return st;
+  float xo = fmaf(vbx, a.dt, xp), yo = fmaf(vby, a.dt, yp), zo = fmaf(vbz, a.dt, zp);
+  float uo = 2.f * vbx - un, vo = 2.f * vby - vn, wo = 2.f * vbz - wn;
+  if (!skipbc) {
+    sk::fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+    sk::fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+    sk::fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+    if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
+        zo > a.hi[2])
+      return ST_RUNAWAY;
+  }
+  xp = xo; yp = yo; zp = zo;
+  un = uo; vn = vo; wn = wo;
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Mover: one warp per bin.  A warp claims kMoveClaim consecutive bins; their
+// cell records (contiguous: records are in cell order) are staged in shared
+// memory by one TMA bulk copy per claim, one claim ahead (double buffer,
+// mbarrier completion).  Stayers are written back in place; each leaver is
+// listed (x..w, q, id, new cell) and leaves a hole; after the bin's last tile
+// the holes below the new count are refilled with the bin's trailing stayers
+// (about as many particle copies as leavers).  The next tile's particles
+// (across bins of the claim) are loaded while the current tile is pushed.
+template <bool RX, bool RY, bool RZ>
+__global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a,
+                                                     const __grid_constant__ Bins b) {
+  __shared__ __align__(128) float4 recs_s[8][2][kMoveClaim * 12];
+  __shared__ __align__(8) unsigned long long bars_s[8][2];
+  __shared__ int holes_s[8][kHoleCap];
+  __shared__ long long lvslot_s[8][kHoleCap];
+  const int wid = threadIdx.x >> 5;
+  const unsigned lane = threadIdx.x & 31;
+  int* const holes = holes_s[wid];
+  long long* const lvslot = lvslot_s[wid];
+  unsigned long long* const bars = bars_s[wid];
+  const unsigned lt = lanemask_lt();
+  const float qe = fabsf(a.qdt2m) * __ldg(a.emax) * 1.00001f;
+  const float4* const rec_g = static_cast<const float4*>(a.rec);
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  fence_proxy_async();
+  __syncwarp();
+  // claim kMoveClaim bins and stage their records into buffer `bf`
+  auto claim = [&](int bf) -> int {
+    unsigned long long c = 0;
+    if (lane == 0) {
+      c = atomicAdd(&b.stat[ST_WORK_MOVE], (unsigned long long)kMoveClaim);
+      if (c < (unsigned long long)b.ncell) {
+        const int nb = min(kMoveClaim, b.ncell - (int)c);
+        const unsigned bytes = (unsigned)nb * 12u * 16u;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[bf], bytes);
+        bulk_load(recs_s[wid][bf], rec_g + (size_t)c * 12, bytes, &bars[bf]);
+      }
+    }
+    return (int)min(__shfl_sync(0xffffffffu, c, 0), (unsigned long long)b.ncell);
+  };
+  // the warp's current chunk of leaver slots [lv_base, lv_base + kLvChunk),
+  // lv_used of them taken (starts "full": the first leaver claims a chunk)
+  long long lv_base = 0, lv_next = 0;
+  int lv_used = kLvChunk;
+  unsigned phase[2] = {0u, 0u};
+  int bf = 0;
+  int c0 = claim(0);
+  // prefetched particle (one per lane) and the slot it came from
+  float n1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int lv_ = b.variant & 3, sv_ = (b.variant >> 2) & 1;
+  auto fetch = [&](long long q, bool ok) {
+    if (ok) {
+      n1[0] = ld_p(b.x + q, lv_); n1[1] = ld_p(b.y + q, lv_); n1[2] = ld_p(b.z + q, lv_);
+      n1[3] = ld_p(b.u + q, lv_); n1[4] = ld_p(b.v + q, lv_); n1[5] = ld_p(b.w + q, lv_);
+    }
+  };
+  float4 R[12];
+  while (c0 < b.ncell) {
+    const int c1 = min(c0 + kMoveClaim, b.ncell);
+    const int cn = claim(bf ^ 1);  // the next claim's records load meanwhile
+    mbar_wait(&bars[bf], phase[bf]);
+    phase[bf] ^= 1u;
+    long long s0 = b.start[c0];
+    int n = (int)min((long long)b.count[c0], b.start[c0 + 1] - s0);
+    fetch(s0 + lane, (int)lane < n);
+    bool pf_ok = true;  // (warp-uniform) n1 holds this bin's first tile
+    Ijk q3 = ijk_of(a, c0);
+    for (int c = c0; c < c1; ++c, q3 = ijk_advance(a, q3, 1)) {
+      // metadata of the next bin of the claim (its first tile is prefetched
+      // during this bin's last tile)
+      long long s1 = 0;
+      int n_1 = 0;
+      if (c + 1 < c1) {
+        s1 = b.start[c + 1];
+        n_1 = (int)min((long long)b.count[c + 1], b.start[c + 2] - s1);
+      }
+      if (n > 0) {
+        if (!pf_ok) fetch(s0 + lane, (int)lane < n);
+        const float4* rs = recs_s[wid][bf] + (c - c0) * 12;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) R[q] = rs[q];
+        const Box bx = cell_box(a, q3);
+        int held = c;
+        int nh = 0;
+#pragma unroll 1
+        for (int t0 = 0; t0 < n; t0 += 32) {
+          const int r = t0 + (int)lane;
+          const bool valid = r < n;
+          const long long p = s0 + r;
+          float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
+          if (t0 + 32 < n) fetch(p + 32, r + 32 < n);
+          else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1);
+          if (n - t0 < 32) {
+            // the lanes past the bin's end push a copy of lane 0's particle
+            // (not stored), so the whole warp runs the push
+            const float c0x = __shfl_sync(0xffffffffu, xp, 0), c0y = __shfl_sync(0xffffffffu, yp, 0);
+            const float c0z = __shfl_sync(0xffffffffu, zp, 0), c0u = __shfl_sync(0xffffffffu, un, 0);
+            const float c0v = __shfl_sync(0xffffffffu, vn, 0), c0w = __shfl_sync(0xffffffffu, wn, 0);
+            if (!valid) {
+              xp = c0x; yp = c0y; zp = c0z; un = c0u; vn = c0v; wn = c0w;
+            }
+          }
+          const bool all_in =
+              __all_sync(0xffffffffu, sk::interior(a, qe, xp, yp, zp, un, vn, wn));
+          const int st = push_bin<RX, RY, RZ>(a, R, held, c, rs, xp, yp, zp, un, vn, wn, all_in);
+          int dest = c;
+          if (st == ST_OK) {
+            const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
+            const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
+            const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
+            if (!in_box(bx, gx, gy, gz)) {
+              const int i = min((int)gx, a.nx - 1), j = min((int)gy, a.ny - 1),
+                        k = min((int)gz, a.nz - 1);
+              dest = i + a.nx * j + a.cny * k;
+            }
+          } else if (valid) {
+            atomicMax(a.status, st);  // not stored (kernels.py:618-621); the cycle raises
+          }
+        const bool leave = valid && st == ST_OK && dest != c;
+        const unsigned L = __ballot_sync(0xffffffffu, leave);
+        bool listed = false;
+        if (L) {
+          // leaver slots from the warp's private chunk of the list (one
+          // global atomic per kLvChunk slots, not one per tile)
+          const int nl = __popc(L);
+          const int rank = __popc(L & lt);
+          if (lv_used + nl > kLvChunk) {
+            // the rest of the current chunk, then a fresh chunk
+            unsigned long long nb = 0;
+            if (lane == 0) nb = atomicAdd(&b.stat[ST_LEAVERS], (unsigned long long)kLvChunk);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+            lv_next = (long long)nb;
+          }
+          const int room = kLvChunk - lv_used;  // slots left in the current chunk
+          const long long slot =
+              rank < room ? lv_base + lv_used + rank : lv_next + (rank - room);
+          // accepted leavers are a prefix in rank order (hole index grows
+          // with the rank), so their hole indices stay contiguous
+          listed = leave && slot < b.lv_cap && nh + rank < kHoleCap;
+          if (listed) {
+            // q and id are added at the end of the bin (one load latency
+            // per bin instead of per tile)
+            float4* rec = reinterpret_cast<float4*>(b.lv + slot);
+            rec[0] = make_float4(xp, yp, zp, un);
+            rec[1] = make_float4(vn, wn, 0.f, __int_as_float(dest));
+            holes[nh + rank] = r;
+            lvslot[nh + rank] = slot;
+          } else if (leave) {
+            // stays here as a misplaced particle (slow paths; host rebuilds)
+            atomicAdd(&b.stat[ST_MISPLACED], 1ULL);
+            if (slot < b.lv_cap) b.lv[slot].b.w = __int_as_float(-1);
+          }
+          nh += __popc(__ballot_sync(0xffffffffu, listed));
+          if (lv_used + nl > kLvChunk) {
+            lv_base = lv_next;
+            lv_used = nl - room;
+          } else {
+            lv_used += nl;
+          }
+        }
+        // every lane of the tile stores (a listed leaver's slot becomes a
+        // hole, refilled below or past the new count), so whole sectors are
+        // written; write-back stores, so the refill and the migration find
+        // the bin's lines in L2
+        if (valid && st == ST_OK) {
+          st_p(b.x + p, xp, sv_); st_p(b.y + p, yp, sv_); st_p(b.z + p, zp, sv_);
+          st_p(b.u + p, un, sv_); st_p(b.v + p, vn, sv_); st_p(b.w + p, wn, sv_);
+        }
+      }
+        __syncwarp();
+        if (nh > 0) {
+          // leavers' q and id into their records; refill: the holes below the
+          // new count take the trailing stayers (holes are ascending; the
+          // k-th trailing stayer is the k-th slot >= n_stay that is not a
+          // hole).  All loads are issued before any store: the refill writes
+          // into leaver slots.
+          const int n_stay = n - nh;
+          int nlow = 0;
+          for (int k0 = 0; k0 < nh; k0 += 32) {
+            const int k = k0 + (int)lane;
+            nlow += __popc(__ballot_sync(0xffffffffu, k < nh && holes[k] < n_stay));
+          }
+          for (int k0 = 0; k0 < nh; k0 += 32) {
+            const int k = k0 + (int)lane;
+            // this lane's leaver (k < nh) and refill pair (k < nlow)
+            float lq = 0.f;
+            long long lid = 0;
+            if (k < nh) {
+              const long long hp = s0 + holes[k];
+              lq = b.q[hp];
+              lid = b.id[hp];
+            }
+            long long src = 0, dst = 0;
+            float rx = 0.f, ry = 0.f, rz = 0.f, ru = 0.f, rv = 0.f, rw = 0.f, rq = 0.f;
+            long long rid = 0;
+            if (k < nlow) {
+              int t = n_stay + k;
+              for (int j = nlow; j < nh; ++j) {
+                if (holes[j] <= t) ++t;
+                else break;
+              }
+              src = s0 + t;
+              dst = s0 + holes[k];
+              rx = b.x[src]; ry = b.y[src]; rz = b.z[src];
+              ru = b.u[src]; rv = b.v[src]; rw = b.w[src];
+              rq = b.q[src]; rid = b.id[src];
+            }
+            if (k < nh) {
+              float* rec = reinterpret_cast<float*>(b.lv + lvslot[k]);
+              rec[6] = lq;
+              *reinterpret_cast<long long*>(rec + 8) = lid;
+            }
+            __syncwarp();
+            if (k < nlow) {
+              b.x[dst] = rx; b.y[dst] = ry; b.z[dst] = rz;
+              b.u[dst] = ru; b.v[dst] = rv; b.w[dst] = rw;
+              b.q[dst] = rq; b.id[dst] = rid;
+            }
+          }
+        if (lane == 0) b.count[c] = n_stay;
+        }
+        __syncwarp();
+      }
+      pf_ok = n > 0 && n_1 > 0;
+      s0 = s1;
+      n = n_1;
+    }
+    __syncwarp();  // every lane is done with buffer bf before it is refilled
+    c0 = cn;
+    bf ^= 1;
+  }
+  // unused slots of the last leaver chunk carry no particle
+  for (int k = lv_used + (int)lane; k < kLvChunk; k += 32)
+    if (lv_base + k < b.lv_cap) b.lv[lv_base + k].b.w = __int_as_float(-1);
+}
+
+// ---------------------------------------------------------------------------
+// Migration: every listed leaver claims a slot at the end of its new bin.
+__global__ void __launch_bounds__(256) migrate_bins(const __grid_constant__ Bins b) {
+  const long long nl = min((long long)b.stat[ST_LEAVERS], b.lv_cap);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+    const Leaver L = b.lv[i];
+    const int dest = __float_as_int(L.b.w);
+    if (dest < 0 || dest >= b.ncell) continue;
+    const int pos = atomicAdd(&b.count[dest], 1);
+    const long long s = b.start[dest];
+    if (pos < b.start[dest + 1] - s) {
+      const long long d = s + pos;
+      b.x[d] = L.a.x; b.y[d] = L.a.y; b.z[d] = L.a.z;
+      b.u[d] = L.a.w; b.v[d] = L.b.x; b.w[d] = L.b.y;
+      b.q[d] = L.b.z; b.id[d] = L.id;
+    } else {
+      const unsigned long long o = atomicAdd(&b.stat[ST_OVERFLOW], 1ULL);
+      if ((long long)o < b.ov_cap) b.ov[o] = L;
+      else atomicAdd(&b.stat[ST_LOST], 1ULL);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deposit of the overflow list and of the particles the deposit found
+// misplaced: one particle straight onto the lattice with the reference's
+// per-contribution rounding (kernels.py:689-734).  Rare.
+__device__ __forceinline__ void deposit_one(const P& a, float x, float y, float z, float u,
+                                            float v, float w, float q) {
+  float fx, fy, fz;
+  int i, j, k;
+  sk::cell_of(a, x, y, z, fx, fy, fz, i, j, k);
+  const float wx[2] = {1.f - fx, fx}, wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+  const float mv[10] = {1.f, u, v, w, u * u, u * v, u * w, v * v, v * w, w * w};
+  for (int c = 0; c < 8; ++c) {
+    const int node = ((i + (c & 1)) * a.NY + (j + ((c >> 1) & 1))) * a.NZ + k + ((c >> 2) & 1);
+    const double iv =
+        (a.iv_d ? __ldg(a.iv_d + node) : (double)__ldg(a.iv_f + node)) * a.scale;
+    const float base = q * wx[c & 1] * wy[(c >> 1) & 1] * wz[(c >> 2) & 1];
+    for (int m = 0; m < 10; ++m) {
+      const long long l = __double2ll_rn((double)(base * mv[m]) * iv);
+      if (l) atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)m * a.NN + node),
+                       (unsigned long long)l);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) deposit_list(const __grid_constant__ P a,
+                                                    const __grid_constant__ Bins b) {
+  const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
+  const long long nl = min((long long)b.stat[ST_LATE], b.late_cap);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < no + nl;
+       i += stride) {
+    const Leaver L = i < no ? b.ov[i] : b.late[i - no];
+    deposit_one(a, L.a.x, L.a.y, L.a.z, L.a.w, L.b.x, L.b.y, L.b.z);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deposit: quarter-warp q (8 lanes) per bin, four bins per warp round.
+// Lane l accumulates for its particles the 80 products q w_c m_k in
+// registers: A[k][cp] holds corners (2cp, 2cp + 1) of moment k, so one FFMA2
+// multiplies a corner pair of bases by a broadcast moment value.  The flush
+// writes each lane's 80 sums as a row of shared memory ([k][c], 20 x
+// STS.128), and lane (q, l) then adds corner l's 10 moments over its
+// quarter's 8 rows (quarter offset 8q: the 32 lanes read 32 distinct banks).
+// The next particle of each lane (same bin, or the next round's bin) is
+// loaded while the current one is accumulated.
+__global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P a,
+                                                       const __grid_constant__ Bins b) {
+  extern __shared__ __align__(16) float dsm[];
+  const unsigned lane = threadIdx.x & 31;
+  const int qd = (int)(lane >> 3), l = (int)(lane & 7);
+  float* const ws = dsm + (threadIdx.x >> 5) * kWarpSm;
+  float* const myrow = ws + lane * kRowS + 8 * qd;
+  const float* const rd = ws + (8 * qd) * kRowS + 8 * qd + l;
+  const int ci_off = l & 1, cj_off = (l >> 1) & 1, ck_off = (l >> 2) & 1;
+  float n1[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int dv_ = 1 + ((b.variant >> 4) & 1);  // read-only path by default (measured)
+  auto fetch = [&](long long q, bool ok) {
+    if (ok) {
+      n1[0] = ld_p(b.x + q, dv_); n1[1] = ld_p(b.y + q, dv_); n1[2] = ld_p(b.z + q, dv_);
+      n1[3] = ld_p(b.u + q, dv_); n1[4] = ld_p(b.v + q, dv_); n1[5] = ld_p(b.w + q, dv_);
+      n1[6] = ld_p(b.q + q, dv_);
+    }
+  };
+  for (;;) {
+    unsigned long long cc = 0;
+    if (lane == 0) cc = atomicAdd(&b.stat[ST_WORK_DEP], (unsigned long long)kDepClaim);
+    cc = __shfl_sync(0xffffffffu, cc, 0);
+    if (cc >= (unsigned long long)b.ncell) break;
+    const int c0 = (int)cc;
+    // this quarter's bin of round 0 and its cell coordinates
+    int c = c0 + qd;
+    Ijk q3 = ijk_of(a, min(c, b.ncell - 1));
+    long long s0 = 0;
+    int n = 0;
+    if (c < b.ncell) {
+      s0 = b.start[c];
+      n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
+    }
+    fetch(s0 + l, l < n);
+#pragma unroll 1
+    for (int rnd = 0; rnd < kDepClaim / 4; ++rnd) {
+      if (c0 + 4 * rnd >= b.ncell) break;
+      const bool okb = c < b.ncell;
+      // next round's bin of this quarter
+      const int cn = c + 4;
+      long long s1 = 0;
+      int n_1 = 0;
+      if (rnd + 1 < kDepClaim / 4 && cn < b.ncell) {
+        s1 = b.start[cn];
+        n_1 = (int)min((long long)b.count[cn], b.start[cn + 1] - s1);
+      }
+      const int nit = (int)__reduce_max_sync(0xffffffffu, (unsigned)((n + 7) >> 3));
+      if (nit == 0) fetch(s1 + l, l < n_1);  // (the loop below prefetches otherwise)
+      const Box bx = cell_box(a, q3);
+      F2 A[10][4];
+#pragma unroll
+      for (int k = 0; k < 10; ++k)
+#pragma unroll
+        for (int cp = 0; cp < 4; ++cp) A[k][cp] = f2(0.f, 0.f);
+#pragma unroll 1
+      for (int it = 0; it < nit; ++it) {
+        const int pi = it * 8 + l;
+        bool valid = pi < n;
+        const float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5],
+                    qp = n1[6];
+        if (it + 1 < nit) fetch(s0 + pi + 8, pi + 8 < n);
+        else fetch(s1 + l, l < n_1);
+        const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
+        const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
+        const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
+        if (valid && !in_box(bx, gx, gy, gz)) {
+          // misplaced (a leaver the mover could not list): the late list
+          const unsigned long long o = atomicAdd(&b.stat[ST_LATE], 1ULL);
+          if ((long long)o < b.late_cap) {
+            Leaver L;
+            L.a = make_float4(xp, yp, zp, un);
+            L.b = make_float4(vn, wn, qp, 0.f);
+            L.id = 0;
+            L.pad = 0;
+            b.late[o] = L;
+          } else {
+            atomicAdd(&b.stat[ST_LOST], 1ULL);
+          }
+          valid = false;
+        }
+        const float qs = valid ? qp : 0.f;
+        const float fx = gx - bx.cf[0], fy = gy - bx.cf[1], fz = gz - bx.cf[2];
+        const F2 Q = f2(qs - qs * fx, qs * fx);  // q (1 - fx), q fx
+        const F2 Qy0 = __fmul2_rn(Q, f2(1.f - fy, 1.f - fy));
+        const F2 Qy1 = __fmul2_rn(Q, f2(fy, fy));
+        const float az = 1.f - fz;
+        F2 Bc[4];
+        Bc[0] = __fmul2_rn(Qy0, f2(az, az));
+        Bc[1] = __fmul2_rn(Qy1, f2(az, az));
+        Bc[2] = __fmul2_rn(Qy0, f2(fz, fz));
+        Bc[3] = __fmul2_rn(Qy1, f2(fz, fz));
+        const float mv[10] = {1.f,     un,      vn,      wn,      un * un,
+                              un * vn, un * wn, vn * vn, vn * wn, wn * wn};
+#pragma unroll
+        for (int cp = 0; cp < 4; ++cp) A[0][cp] = __fadd2_rn(A[0][cp], Bc[cp]);
+#pragma unroll
+        for (int k = 1; k < 10; ++k)
+#pragma unroll
+          for (int cp = 0; cp < 4; ++cp) A[k][cp] = fma2(Bc[cp], f2(mv[k], mv[k]), A[k][cp]);
+      }
+      if (nit > 0) {
+        // ---- flush: transpose through shared memory, then one corner per lane
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+          reinterpret_cast<float4*>(myrow + 8 * k)[0] =
+              make_float4(A[k][0].x, A[k][0].y, A[k][1].x, A[k][1].y);
+          reinterpret_cast<float4*>(myrow + 8 * k)[1] =
+              make_float4(A[k][2].x, A[k][2].y, A[k][3].x, A[k][3].y);
+        }
+        __syncwarp();
+        float sm[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) sm[k] = 0.f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) sm[k] += rd[r * kRowS + 8 * k];
+        __syncwarp();
+        if (okb && n > 0) {
+          const int node = ((q3.i + ci_off) * a.NY + (q3.j + cj_off)) * a.NZ + q3.k + ck_off;
+          const double iv =
+              (a.iv_d ? __ldg(a.iv_d + node) : (double)__ldg(a.iv_f + node)) * a.scale;
+          unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.acc + node);
+#pragma unroll
+          for (int m = 0; m < 10; ++m) {
+            if (sm[m] != 0.f)
+              atomicAdd(dst + (size_t)m * a.NN,
+                        (unsigned long long)__double2ll_rn((double)sm[m] * iv));
+          }
+        }
+      }
+      c = cn;
+      q3 = ijk_advance(a, q3, 4);
+      s0 = s1;
+      n = n_1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Build: fast-f32 cell keys (cell_of), histogram, capacities, stable scatter.
+__global__ void bin_keys(const P a, const float* __restrict__ x, const float* __restrict__ y,
+                         const float* __restrict__ z, long long n, unsigned* keys,
+                         unsigned* idx, int* hist, int* bad) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    const float gx = fmaf(x[p], a.idx[0], -a.ogs[0]);
+    const float gy = fmaf(y[p], a.idx[1], -a.ogs[1]);
+    const float gz = fmaf(z[p], a.idx[2], -a.ogs[2]);
+    int c = 0;
+    if (!(gx > -1.f && gy > -1.f && gz > -1.f)) {
+      *bad = 1;
+    } else {
+      const int i = min((int)gx, a.nx - 1), j = min((int)gy, a.ny - 1),
+                k = min((int)gz, a.nz - 1);
+      c = i + a.nx * j + a.cny * k;
+    }
+    if (keys) keys[p] = (unsigned)c;
+    if (idx) idx[p] = (unsigned)p;
+    if (hist) atomicAdd(hist + c, 1);
+  }
+}
+
+__global__ void bin_caps(const int* __restrict__ cnt, int ncell, float frac, int smin,
+                         long long* cap) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncell; c += stride) {
+    if (c == ncell) {
+      cap[c] = 0;
+      continue;
+    }
+    const int n = cnt[c];
+    // multiples of 8 slots: every bin starts on a 32-byte sector
+    cap[c] = ((long long)n + max(smin, (int)ceilf(frac * (float)n)) + 7) & ~7LL;
+  }
+}
+
+// sorted position r -> slot start[key] + (r - first[key]); first = exclusive
+// scan of the counts
+__global__ void bin_scatter(const unsigned* __restrict__ skeys,
+                            const unsigned* __restrict__ sidx, long long n,
+                            const long long* __restrict__ start,
+                            const long long* __restrict__ first, const float* const* src,
+                            const long long* __restrict__ sid, float* const* dst,
+                            long long* __restrict__ did) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const unsigned k = skeys[r], j = sidx[r];
+    const long long d = start[k] + (r - first[k]);
+#pragma unroll
+    for (int a = 0; a < 7; ++a) dst[a][d] = src[a][j];
+    did[d] = sid[j];
+  }
+}
+
+// export: bin c's live particles to flat[off[c] ...]
+__global__ void bin_export(const __grid_constant__ Bins b, const long long* __restrict__ off,
+                           float* const* dst, long long* __restrict__ did) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const float* src[7] = {b.x, b.y, b.z, b.u, b.v, b.w, b.q};
+  for (long long c = gw; c < b.ncell; c += nw) {
+    const long long s0 = b.start[c];
+    const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
+    const long long o = off[c];
+    for (int r = lane; r < n; r += 32) {
+#pragma unroll
+      for (int a = 0; a < 7; ++a) dst[a][o + r] = src[a][s0 + r];
+      did[o + r] = b.id[s0 + r];
+    }
+  }
+}
+
+// the overflow list appended after the bins' particles
+__global__ void list_export(const __grid_constant__ Bins b, long long o0, float* const* dst,
+                            long long* __restrict__ did) {
+  const long long n = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const Leaver L = b.ov[i];
+    const long long d = o0 + i;
+    dst[0][d] = L.a.x; dst[1][d] = L.a.y; dst[2][d] = L.a.z; dst[3][d] = L.a.w;
+    dst[4][d] = L.b.x; dst[5][d] = L.b.y; dst[6][d] = L.b.z;
+    did[d] = L.id;
+  }
+}
+
+__global__ void clamp_counts(int* cnt, const long long* start, int ncell) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += stride) {
+    const long long cap = start[c + 1] - start[c];
+    if (cnt[c] > cap) cnt[c] = (int)cap;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Re-slack (the cheap rebuild after an overflow): new capacities from the
+// live counts plus the overflow list's arrivals, then every bin is copied to
+// its new place and the overflow list appended (no sort: the bins are
+// already in cell order).
+__global__ void reslack_counts(const __grid_constant__ Bins b, int* __restrict__ ncount) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < b.ncell; c += stride)
+    ncount[c] = (int)min((long long)b.count[c], b.start[c + 1] - b.start[c]);
+}
+__global__ void reslack_hist(const __grid_constant__ Bins b, int* __restrict__ ncount) {
+  const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < no; i += stride) {
+    const int dest = __float_as_int(b.ov[i].b.w);
+    if (dest >= 0 && dest < b.ncell) atomicAdd(ncount + dest, 1);
+  }
+}
+// warp per bin: live particles to the new layout; ncount = live count
+__global__ void reslack_copy(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
+                             int* __restrict__ ncount, float* const* dst,
+                             long long* __restrict__ did) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const float* src[7] = {b.x, b.y, b.z, b.u, b.v, b.w, b.q};
+  for (long long c = gw; c < b.ncell; c += nw) {
+    const long long s0 = b.start[c];
+    const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
+    const long long d0 = nstart[c];
+    for (int r = lane; r < n; r += 32) {
+#pragma unroll
+      for (int a = 0; a < 7; ++a) __stcs(dst[a] + d0 + r, __ldcs(src[a] + s0 + r));
+      __stcs(did + d0 + r, __ldcs(b.id + s0 + r));
+    }
+    if (lane == 0) ncount[c] = n;
+  }
+}
+__global__ void reslack_place(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
+                              int* __restrict__ ncount, float* const* dst,
+                              long long* __restrict__ did) {
+  const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < no; i += stride) {
+    const Leaver L = b.ov[i];
+    const int dest = __float_as_int(L.b.w);
+    if (dest < 0 || dest >= b.ncell) continue;
+    const long long d = nstart[dest] + atomicAdd(ncount + dest, 1);
+    dst[0][d] = L.a.x; dst[1][d] = L.a.y; dst[2][d] = L.a.z; dst[3][d] = L.a.w;
+    dst[4][d] = L.b.x; dst[5][d] = L.b.y; dst[6][d] = L.b.z;
+    did[d] = L.id;
+  }
+}
+
+}  // namespace bins
+
+namespace {
+
+int bcheck(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
+
+int nsm() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <typename K>
+int resident_grid(K k, size_t smem) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  return nsm() * (per_sm < 1 ? 1 : per_sm);
+}
+
+template <bool RX, bool RY, bool RZ>
+int launch_mover_bins(const bins::P& a, const bins::Bins& b, cudaStream_t s) {
+  auto k = bins::mover_bins<RX, RY, RZ>;
+  const int g = resident_grid(k, 0);
+  const int th = timing_begin(TK_MOVER, s);
+  k<<<g, 256, 0, s>>>(a, b);
+  timing_end(th, s);
+  note_launch();
+  return bcheck("mover_bins launch");
+}
+
+int launch_mover_bins_any(const bins::P& a, const bins::Bins& b, const int64_t* geo_i,
+                          cudaStream_t s) {
+  switch ((geo_i[3] ? 1 : 0) | (geo_i[4] ? 2 : 0) | (geo_i[5] ? 4 : 0)) {
+    case 0: return launch_mover_bins<false, false, false>(a, b, s);
+    case 1: return launch_mover_bins<true, false, false>(a, b, s);
+    case 2: return launch_mover_bins<false, true, false>(a, b, s);
+    case 3: return launch_mover_bins<true, true, false>(a, b, s);
+    case 4: return launch_mover_bins<false, false, true>(a, b, s);
+    case 5: return launch_mover_bins<true, false, true>(a, b, s);
+    case 6: return launch_mover_bins<false, true, true>(a, b, s);
+    default: return launch_mover_bins<true, true, true>(a, b, s);
+  }
+}
+
+}  // namespace
+
+// One cycle of one species on the binned layout: mover, migration, deposit
+// (+ the overflow and late lists).  The stat words are zeroed here; the host
+// reads them after the cycle (overflow / misplaced -> rebuild, lost -> error).
+int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
+  bins::P a;
+  fill_params<float>(c, a);
+  a.rec = c.records;
+  a.emax = reinterpret_cast<const float*>(
+      (const char*)c.records + (split_records_bytes(4, c.geo_i) - 32));
+  bins::Bins b;
+  b.x = (float*)c.x; b.y = (float*)c.y; b.z = (float*)c.z;
+  b.u = (float*)c.u; b.v = (float*)c.v; b.w = (float*)c.w;
+  b.q = (float*)const_cast<void*>(c.q);
+  b.id = (long long*)ba.ids;
+  b.start = (const long long*)ba.start;
+  b.count = ba.count;
+  b.ncell = (int)ba.ncell;
+  b.lv = (bins::Leaver*)ba.leavers;
+  b.lv_cap = ba.leaver_cap;
+  b.ov = (bins::Leaver*)ba.overflow;
+  b.ov_cap = ba.overflow_cap;
+  b.late = (bins::Leaver*)ba.late;
+  b.late_cap = ba.late_cap;
+  b.stat = (unsigned long long*)ba.stat;
+  static const int variant = [] {
+    const char* e = getenv("BP_BINS_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  b.variant = variant;
+  cudaMemsetAsync(b.stat, 0, bins::ST_N * sizeof(unsigned long long), s);
+  int rc = launch_mover_bins_any(a, b, c.geo_i, s);
+  if (rc) return rc;
+  bins::migrate_bins<<<nsm() * 8, 256, 0, s>>>(b);
+  note_launch();
+  if ((rc = bcheck("migrate_bins launch"))) return rc;
+  const size_t smem = (size_t)8 * bins::kWarpSm * sizeof(float);
+  static bool attr[64] = {};
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(bins::deposit_bins, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int g = resident_grid(bins::deposit_bins, smem);
+  const int th = timing_begin(TK_DEPOSIT, s);
+  bins::deposit_bins<<<g, 256, smem, s>>>(a, b);
+  timing_end(th, s);
+  note_launch();
+  if ((rc = bcheck("deposit_bins launch"))) return rc;
+  bins::deposit_list<<<nsm(), 256, 0, s>>>(a, b);
+  note_launch();
+  return bcheck("deposit_list launch");
+}
+
+// Build step 1: cell histogram and bin layout (start = exclusive scan of the
+// capacities); returns the total slot count through *total (synchronises).
+int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin,
+              int64_t* total, cudaStream_t s) {
+  bins::P a;
+  fill_params<float>(c, a);
+  const int ncell = a.nx * a.ny * a.nz;
+  const long long n = c.count;
+  cudaMemsetAsync(count, 0, (size_t)ncell * sizeof(int), s);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (long long*)nullptr, (long long*)nullptr,
+                                ncell + 1, s);
+  int* bad = nullptr;
+  long long* caps = nullptr;
+  void* tmp = nullptr;
+  if (cudaMallocAsync(&bad, 16, s) != cudaSuccess ||
+      cudaMallocAsync(&caps, (size_t)(ncell + 1) * 8, s) != cudaSuccess ||
+      cudaMallocAsync(&tmp, tmp_bytes + 16, s) != cudaSuccess) {
+    set_error("bins_plan: scratch allocation failed");
+    return -2;
+  }
+  cudaMemsetAsync(bad, 0, 16, s);
+  if (n > 0) {
+    bins::bin_keys<<<nsm() * 8, 256, 0, s>>>(a, (const float*)c.x + c.start,
+                                             (const float*)c.y + c.start,
+                                             (const float*)c.z + c.start, n, nullptr, nullptr,
+                                             count, bad);
+    note_launch();
+  }
+  bins::bin_caps<<<nsm() * 4, 256, 0, s>>>(count, ncell, (float)frac, smin, caps);
+  note_launch();
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, caps, (long long*)start, ncell + 1, s);
+  int hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(total, start + ncell, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(bad, s);
+  cudaFreeAsync(caps, s);
+  cudaFreeAsync(tmp, s);
+  int rc = bcheck("bins_plan");
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_plan sync");
+  if (rc) return rc;
+  return hbad ? 3 : 0;
+}
+
+// Build step 2: stable scatter of the flat span into the planned bins.
+int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* const* dst,
+              int64_t* dst_ids, cudaStream_t s) {
+  bins::P a;
+  fill_params<float>(c, a);
+  const int ncell = a.nx * a.ny * a.nz;
+  const long long n = c.count;
+  if (n <= 0) return 0;
+  if (n > 0xffffffffLL) {
+    set_error("bins_fill: %lld particles exceed the 32-bit index space", n);
+    return -1;
+  }
+  int end_bit = 1;
+  while (end_bit < 32 && (1LL << end_bit) < ncell) ++end_bit;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned*)nullptr, (unsigned*)nullptr,
+                                  (unsigned*)nullptr, (unsigned*)nullptr, n, 0, end_bit, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (long long*)nullptr, ncell,
+                                s);
+  auto up = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t nb = up((size_t)n * 4);
+  const size_t need = 4 * nb + up((size_t)ncell * 4) + up((size_t)ncell * 8) + up(16) +
+                      up(sort_bytes) + up(scan_bytes) + up(16 * sizeof(void*));
+  char* ws = nullptr;
+  if (cudaMallocAsync(&ws, need, s) != cudaSuccess) {
+    set_error("bins_fill: scratch allocation failed");
+    return -2;
+  }
+  char* p = ws;
+  unsigned* k_in = (unsigned*)p; p += nb;
+  unsigned* k_out = (unsigned*)p; p += nb;
+  unsigned* i_in = (unsigned*)p; p += nb;
+  unsigned* i_out = (unsigned*)p; p += nb;
+  int* hist = (int*)p; p += up((size_t)ncell * 4);
+  long long* first = (long long*)p; p += up((size_t)ncell * 8);
+  int* bad = (int*)p; p += up(16);
+  void* sort_tmp = p; p += up(sort_bytes);
+  void* scan_tmp = p; p += up(scan_bytes);
+  void** ptrs = (void**)p;
+  cudaMemsetAsync(hist, 0, (size_t)ncell * 4, s);
+  cudaMemsetAsync(bad, 0, 16, s);
+  bins::bin_keys<<<nsm() * 8, 256, 0, s>>>(a, (const float*)c.x + c.start,
+                                           (const float*)c.y + c.start,
+                                           (const float*)c.z + c.start, n, k_in, i_in, hist, bad);
+  note_launch();
+  cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, k_in, k_out, i_in, i_out, n, 0, end_bit,
+                                  s);
+  cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, hist, first, ncell, s);
+  const void* hp[16] = {(const float*)c.x + c.start, (const float*)c.y + c.start,
+                        (const float*)c.z + c.start, (const float*)c.u + c.start,
+                        (const float*)c.v + c.start, (const float*)c.w + c.start,
+                        (const float*)c.q + c.start, dst[0], dst[1], dst[2], dst[3], dst[4],
+                        dst[5], dst[6], nullptr, nullptr};
+  cudaMemcpyAsync(ptrs, hp, sizeof(hp), cudaMemcpyHostToDevice, s);
+  bins::bin_scatter<<<nsm() * 8, 256, 0, s>>>(k_out, i_out, n, (const long long*)start, first,
+                                              (const float* const*)ptrs,
+                                              (const long long*)src_ids + c.start,
+                                              (float* const*)(ptrs + 7), (long long*)dst_ids);
+  note_launch();
+  cudaFreeAsync(ws, s);
+  int rc = bcheck("bins_fill");
+  // the host array hp must outlive the async copy
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_fill sync");
+  return rc;
+}
+
+// Live-particle offsets of the bins (exclusive scan of the clamped counts)
+// and the flat copy; the overflow list follows at the end.  Returns the
+// particle total through *total (synchronises).
+int bins_export(const BinsArgs& ba, void* const* src, int64_t* offsets, void* const* dst,
+                int64_t* dst_ids, int64_t* total, cudaStream_t s) {
+  bins::Bins b{};
+  b.x = (float*)src[0]; b.y = (float*)src[1]; b.z = (float*)src[2];
+  b.u = (float*)src[3]; b.v = (float*)src[4]; b.w = (float*)src[5];
+  b.q = (float*)src[6];
+  b.id = (long long*)ba.ids;
+  b.start = (const long long*)ba.start;
+  b.count = ba.count;
+  b.ncell = (int)ba.ncell;
+  b.ov = (bins::Leaver*)ba.overflow;
+  b.ov_cap = ba.overflow_cap;
+  b.stat = (unsigned long long*)ba.stat;
+  const int ncell = b.ncell;
+  bins::clamp_counts<<<nsm() * 4, 256, 0, s>>>(ba.count, b.start, ncell);
+  note_launch();
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (long long*)nullptr,
+                                ncell + 1, s);
+  void* tmp = nullptr;
+  int* cnt1 = nullptr;
+  if (cudaMallocAsync(&tmp, scan_bytes + 16, s) != cudaSuccess ||
+      cudaMallocAsync(&cnt1, (size_t)(ncell + 1) * 4, s) != cudaSuccess) {
+    set_error("bins_export: scratch allocation failed");
+    return -2;
+  }
+  cudaMemsetAsync(cnt1 + ncell, 0, 4, s);
+  cudaMemcpyAsync(cnt1, ba.count, (size_t)ncell * 4, cudaMemcpyDeviceToDevice, s);
+  cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, cnt1, (long long*)offsets, ncell + 1, s);
+  long long nb = 0;
+  unsigned long long st[bins::ST_N] = {};
+  cudaMemcpyAsync(&nb, offsets + ncell, 8, cudaMemcpyDeviceToHost, s);
+  if (ba.stat) cudaMemcpyAsync(st, ba.stat, sizeof(st), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return bcheck("bins_export sync");
+  const long long nov =
+      ba.overflow ? std::min((long long)st[bins::ST_OVERFLOW], (long long)ba.overflow_cap) : 0LL;
+  *total = nb + nov;
+  if (!dst) {
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(cnt1, s);
+    return bcheck("bins_export");
+  }
+  void** ptrs = nullptr;
+  cudaMallocAsync(&ptrs, 8 * sizeof(void*), s);
+  cudaMemcpyAsync(ptrs, dst, 7 * sizeof(void*), cudaMemcpyHostToDevice, s);
+  bins::bin_export<<<nsm() * 8, 256, 0, s>>>(b, (const long long*)offsets, (float* const*)ptrs,
+                                             (long long*)dst_ids);
+  note_launch();
+  if (nov > 0) {
+    bins::list_export<<<nsm(), 256, 0, s>>>(b, nb, (float* const*)ptrs, (long long*)dst_ids);
+    note_launch();
+  }
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(cnt1, s);
+  cudaFreeAsync(ptrs, s);
+  int rc = bcheck("bins_export");
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_export sync");
+  return rc;
+}
+
+}  // namespace bp
+
+namespace bp {
+
+namespace {
+bins::Bins bins_of(const BinsArgs& ba, void* const* src) {
+  bins::Bins b{};
+  b.x = (float*)src[0]; b.y = (float*)src[1]; b.z = (float*)src[2];
+  b.u = (float*)src[3]; b.v = (float*)src[4]; b.w = (float*)src[5];
+  b.q = (float*)src[6];
+  b.id = (long long*)ba.ids;
+  b.start = (const long long*)ba.start;
+  b.count = ba.count;
+  b.ncell = (int)ba.ncell;
+  b.ov = (bins::Leaver*)ba.overflow;
+  b.ov_cap = ba.overflow_cap;
+  b.stat = (unsigned long long*)ba.stat;
+  return b;
+}
+}  // namespace
+
+// Re-slack plan: ncount = live + overflow arrivals per bin, nstart = exclusive
+// scan of the padded capacities; *total = nstart[ncell] (synchronises).
+int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t* nstart,
+                      double frac, int smin, int64_t* total, cudaStream_t s) {
+  const bins::Bins b = bins_of(ba, src);
+  const int ncell = b.ncell;
+  bins::reslack_counts<<<nsm() * 4, 256, 0, s>>>(b, ncount);
+  note_launch();
+  bins::reslack_hist<<<nsm() * 2, 256, 0, s>>>(b, ncount);
+  note_launch();
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (long long*)nullptr, (long long*)nullptr,
+                                ncell + 1, s);
+  long long* caps = nullptr;
+  void* tmp = nullptr;
+  if (cudaMallocAsync(&caps, (size_t)(ncell + 1) * 8, s) != cudaSuccess ||
+      cudaMallocAsync(&tmp, tmp_bytes + 16, s) != cudaSuccess) {
+    set_error("bins_reslack_plan: scratch allocation failed");
+    return -2;
+  }
+  bins::bin_caps<<<nsm() * 4, 256, 0, s>>>(ncount, ncell, (float)frac, smin, caps);
+  note_launch();
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, caps, (long long*)nstart, ncell + 1, s);
+  cudaMemcpyAsync(total, nstart + ncell, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(caps, s);
+  cudaFreeAsync(tmp, s);
+  int rc = bcheck("bins_reslack_plan");
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_reslack_plan sync");
+  return rc;
+}
+
+// Re-slack copy into dst (nstart from the plan); ncount ends as the new
+// live counts (synchronises).
+int bins_reslack_copy(const BinsArgs& ba, void* const* src, const int64_t* nstart, int* ncount,
+                      void* const* dst, int64_t* dst_ids, cudaStream_t s) {
+  const bins::Bins b = bins_of(ba, src);
+  void** ptrs = nullptr;
+  if (cudaMallocAsync(&ptrs, 8 * sizeof(void*), s) != cudaSuccess) {
+    set_error("bins_reslack_copy: scratch allocation failed");
+    return -2;
+  }
+  cudaMemcpyAsync(ptrs, dst, 7 * sizeof(void*), cudaMemcpyHostToDevice, s);
+  bins::reslack_copy<<<nsm() * 8, 256, 0, s>>>(b, (const long long*)nstart, ncount,
+                                               (float* const*)ptrs, (long long*)dst_ids);
+  note_launch();
+  bins::reslack_place<<<nsm() * 2, 256, 0, s>>>(b, (const long long*)nstart, ncount,
+                                                (float* const*)ptrs, (long long*)dst_ids);
+  note_launch();
+  cudaFreeAsync(ptrs, s);
+  int rc = bcheck("bins_reslack_copy");
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_reslack_copy sync");
+  return rc;
+}
+
+}  // namespace bp

@@ -653,3 +653,136 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Cell-binned f32 fast path (bp_bins.cu)
+namespace {
+int bins_call(Call& c, int fbytes, const void* xs, const void* ys, const void* zs,
+              const void* us, const void* vs, const void* ws, const void* qs, int64_t start,
+              int64_t count, const double* geo_f, const double* geo_g, const int64_t* geo_i) {
+  if (fbytes != 4 && fbytes != 8) {
+    set_error("unsupported field dtype (%d bytes)", fbytes);
+    return BP_EINVAL;
+  }
+  int rc = check_geo(geo_g, geo_i);
+  if (rc) return rc;
+  if (!geo_f) {
+    set_error("geo_f required");
+    return BP_EINVAL;
+  }
+  c.op = OP_FUSED;
+  c.pbytes = 4; c.fbytes = fbytes;
+  c.x = const_cast<void*>(xs); c.y = const_cast<void*>(ys); c.z = const_cast<void*>(zs);
+  c.u = const_cast<void*>(us); c.v = const_cast<void*>(vs); c.w = const_cast<void*>(ws);
+  c.q = qs;
+  c.start = start; c.count = count;
+  fill_geo(c, geo_f, geo_g, geo_i);
+  ensure_pool();
+  return BP_OK;
+}
+}  // namespace
+
+int bp_bins_leaver_bytes(void) { return bp::kBinsLeaverBytes; }
+
+int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+                 const double* geo_f, const double* geo_g, const int64_t* geo_i,
+                 double slack_frac, int slack_min, int32_t* count, int64_t* start,
+                 int64_t* total, void* stream) {
+  Call c{};
+  int rc = bins_call(c, fbytes, xs, ys, zs, nullptr, nullptr, nullptr, nullptr, 0, n, geo_f,
+                     geo_g, geo_i);
+  if (rc) return rc;
+  if (!count || !start || !total || n < 0 || slack_frac < 0 || slack_min < 0) {
+    set_error("bins_plan: bad arguments");
+    return BP_EINVAL;
+  }
+  return bins_plan(c, count, start, slack_frac, slack_min, total, (cudaStream_t)stream);
+}
+
+int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
+                 const void* vs, const void* ws, const void* qs, const int64_t* ids, int64_t n,
+                 const double* geo_f, const double* geo_g, const int64_t* geo_i,
+                 const int64_t* start, void* const* dst, int64_t* dst_ids, void* stream) {
+  Call c{};
+  int rc = bins_call(c, fbytes, xs, ys, zs, us, vs, ws, qs, 0, n, geo_f, geo_g, geo_i);
+  if (rc) return rc;
+  if (!ids || !start || !dst || !dst_ids || !qs) {
+    set_error("bins_fill: bad arguments");
+    return BP_EINVAL;
+  }
+  for (int k = 0; k < 7; ++k)
+    if (!dst[k]) {
+      set_error("bins_fill: destination array %d missing", k);
+      return BP_EINVAL;
+    }
+  return bins_fill(c, ids, start, dst, dst_ids, (cudaStream_t)stream);
+}
+
+int bp_bins_cycle(int fbytes, float* xs, float* ys, float* zs, float* us, float* vs, float* ws,
+                  float* qs, int64_t* ids, const int64_t* start, int32_t* count, int64_t ncell,
+                  void* leavers, int64_t leaver_cap, void* overflow, int64_t overflow_cap,
+                  void* late, int64_t late_cap, uint64_t* stat, const void* records,
+                  int64_t* acc, const void* invvol,
+                  const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
+                  double dth, double qdt2m, double beta, double one, int n_iters, double scale,
+                  int* d_status, void* stream) {
+  Call c{};
+  int rc = bins_call(c, fbytes, xs, ys, zs, us, vs, ws, qs, 0, 0, geo_f, geo_g, geo_i);
+  if (rc) return rc;
+  if (!records || ((uintptr_t)records % 32) != 0 || !acc || !invvol || !ids || !start ||
+      !count || !stat || !leavers || !overflow || !late || leaver_cap < 0 ||
+      overflow_cap < 0 || late_cap < 0 ||
+      n_iters < 0 || !d_status) {
+    set_error("bins_cycle: bad arguments (records 32-byte aligned, buffers, d_status required)");
+    return BP_EINVAL;
+  }
+  if (ncell != geo_i[0] * geo_i[1] * geo_i[2]) {
+    set_error("bins_cycle: ncell does not match geo_i");
+    return BP_EINVAL;
+  }
+  c.acc = acc; c.invvol = invvol;
+  c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
+  c.n_iters = n_iters; c.mixed = fbytes == 8; c.apply_bc = 1;
+  c.records = records;
+  c.status = d_status;
+  BinsArgs ba{ids,      start,        count, ncell, leavers, leaver_cap,
+              overflow, overflow_cap, stat,  late,  late_cap};
+  return bins_cycle(c, ba, (cudaStream_t)stream);
+}
+
+int bp_bins_export(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+                   int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
+                   int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
+                   void* stream) {
+  if (!src || !ids || !start || !count || !offsets || !total || ncell <= 0) {
+    set_error("bins_export: bad arguments");
+    return BP_EINVAL;
+  }
+  ensure_pool();
+  BinsArgs ba{ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
+              overflow ? overflow_cap : 0, stat, nullptr, 0};
+  return bins_export(ba, (void* const*)src, offsets, dst, dst_ids, total, (cudaStream_t)stream);
+}
+
+int bp_bins_reslack(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
+                    double slack_frac, int slack_min, int32_t* new_count, int64_t* new_start,
+                    void* const* dst, int64_t* dst_ids, int64_t* total, void* stream) {
+  if (!src || !ids || !start || !count || !new_count || !new_start || !total || ncell <= 0 ||
+      slack_frac < 0 || slack_min < 0 || (overflow && !stat)) {
+    set_error("bins_reslack: bad arguments");
+    return BP_EINVAL;
+  }
+  ensure_pool();
+  BinsArgs ba{ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
+              overflow ? overflow_cap : 0, stat, nullptr, 0};
+  if (!dst)
+    return bins_reslack_plan(ba, (void* const*)src, new_count, new_start, slack_frac, slack_min,
+                             total, (cudaStream_t)stream);
+  if (!dst_ids) {
+    set_error("bins_reslack: dst_ids required with dst");
+    return BP_EINVAL;
+  }
+  return bins_reslack_copy(ba, (void* const*)src, new_start, new_count, dst, dst_ids,
+                           (cudaStream_t)stream);
+}

@@ -157,4 +157,11 @@ __device__ __forceinline__ void tri_pair(const double4& A, const double4& B, con
 }
 
 }  // namespace sk
+
+struct Call;
+// Params of one span call (bp_split.cu): geometry, scalars and pointers of
+// `c`; the per-call scratch fields (work, skip, rec, emax) are left null.
+template <typename T>
+void fill_params(const Call& c, sk::Params<T>& a);
+
 }  // namespace bp

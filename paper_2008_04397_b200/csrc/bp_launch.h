@@ -44,6 +44,33 @@ int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
                        const int64_t* geo_i, void* rec, cudaStream_t s);
 int split_fused(const Call& c, const void* rec, cudaStream_t s);
 
+// Cell-binned f32 fast path (bp_bins.cu): the bin layout of one species
+struct BinsArgs {
+  int64_t* ids;
+  const int64_t* start;  // [ncell + 1] slot offsets
+  int* count;            // [ncell] live particles per bin
+  int64_t ncell;
+  void* leavers;         // leaver list (bins_leaver_bytes() each)
+  int64_t leaver_cap;
+  void* overflow;        // overflow list (same records)
+  int64_t overflow_cap;
+  uint64_t* stat;        // [8] counters (bp_b200.h BP_BINS_STAT_*)
+  void* late;            // misplaced particles met by the deposit (same records)
+  int64_t late_cap;
+};
+constexpr int kBinsLeaverBytes = 48;
+int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s);
+int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
+              cudaStream_t s);
+int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* const* dst,
+              int64_t* dst_ids, cudaStream_t s);
+int bins_export(const BinsArgs& ba, void* const* src, int64_t* offsets, void* const* dst,
+                int64_t* dst_ids, int64_t* total, cudaStream_t s);
+int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t* nstart,
+                      double frac, int smin, int64_t* total, cudaStream_t s);
+int bins_reslack_copy(const BinsArgs& ba, void* const* src, const int64_t* nstart, int* ncount,
+                      void* const* dst, int64_t* dst_ids, cudaStream_t s);
+
 // count of kernels this library launched (bp_kernel_launches)
 void note_launch(int n = 1);
 

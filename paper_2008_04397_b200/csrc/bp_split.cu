@@ -722,9 +722,13 @@ int launch_pair(const sk::Params<T>& a, const int64_t* geo_i, cudaStream_t s) {
   return rc ? rc : launch_deposit<T>(a, s);
 }
 
+}  // namespace
+
+// kernel parameters of one span call (geometry, scalars, pointers); the
+// per-call scratch (work counter, skip bitmask, records) is the caller's
 template <typename T>
-int split_fused(const Call& c, const void* rec_in, cudaStream_t s) {
-  sk::Params<T> a;
+void fill_params(const Call& c, sk::Params<T>& a) {
+  a = sk::Params<T>{};
   a.x = (T*)c.x; a.y = (T*)c.y; a.z = (T*)c.z;
   a.u = (T*)c.u; a.v = (T*)c.v; a.w = (T*)c.w;
   a.q = (const T*)c.q;
@@ -751,6 +755,16 @@ int split_fused(const Call& c, const void* rec_in, cudaStream_t s) {
   a.scale = c.scale;
   a.n_iters = c.n_iters;
   a.status = c.status;
+}
+template void fill_params<float>(const Call&, sk::Params<float>&);
+template void fill_params<double>(const Call&, sk::Params<double>&);
+
+namespace {
+
+template <typename T>
+int split_fused(const Call& c, const void* rec_in, cudaStream_t s) {
+  sk::Params<T> a;
+  fill_params<T>(c, a);
   void* rec = const_cast<void*>(rec_in);
   const size_t rbytes = split_records_bytes((int)sizeof(T), c.geo_i);
   // one bit per particle, +2 words of slack

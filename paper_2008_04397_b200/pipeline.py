@@ -96,6 +96,11 @@ class DeviceSimulation:
     # "all": every rank ends the cycle with the summed moments (all-reduce);
     # "root": only rank 0 (where the host solve runs) gets them (reduce)
     reduce: str = "all"
+    # particle layout: "flat" (the reference's SoA, sorted every sort_period
+    # cycles) or "bins" (per-cell bins kept sorted every cycle, bins.py; f32
+    # particles with the fast arithmetic); "auto" picks bins where they apply
+    layout: str = "auto"
+    bin_slack: tuple = (0.5, 32)
 
     def __post_init__(self):
         import torch
@@ -113,7 +118,16 @@ class DeviceSimulation:
         self.acc = [torch.zeros((N_MOMENTS,) + self.geom.node_shape, dtype=torch.int64,
                                 device=self.device) for _ in self.species]
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.particles = [None] * len(self.species)
+        self._flat = [None] * len(self.species)
+        self._bins = [None] * len(self.species)
+        self._lists = None
+        self._flat_cache = None
+        binnable = self.arith == "fast" and pd == torch.float32
+        if self.layout not in ("auto", "flat", "bins"):
+            raise ConfigurationError(f"layout must be auto, flat or bins, not {self.layout!r}")
+        if self.layout == "bins" and not binnable:
+            raise ConfigurationError("the binned layout needs f32 particles and fast arithmetic")
+        self.binned = self.layout == "bins" or (self.layout == "auto" and binnable)
         self.cycle = 0
         from .kernels import make_geo_arrays, kernel_scalars
         npd, nfd = self.precision.particle_dtype, self.precision.field_dtype
@@ -146,7 +160,31 @@ class DeviceSimulation:
         """Install this rank's shard (a DeviceParticles) of species ``sid``."""
         if parts.dtype != self.pdt:
             raise ConfigurationError("particle dtype does not match the precision mode")
-        self.particles[sid] = parts
+        self._flat_cache = None
+        if not self.binned:
+            self._flat[sid] = parts
+            return
+        from .bins import BinnedSpecies, TransitLists
+        self._bins[sid] = BinnedSpecies(parts, self.geom, self.geo_f, self.geo_g, self.geo_i,
+                                        self.E.element_size(), slack=self.bin_slack)
+        n_max = max(b.n for b in self._bins if b is not None)
+        if self._lists is None or self._lists.leaver_cap < int(n_max * 0.25) + (1 << 20):
+            self._lists = TransitLists(self.device, n_max)
+
+    @property
+    def particles(self):
+        """Per-species DeviceParticles of this rank (the binned layout exports
+        its live particles in cell order; cached until the next cycle)."""
+        if not self.binned:
+            return self._flat
+        if self._flat_cache is None:
+            self._flat_cache = [b.flat() if b is not None else None for b in self._bins]
+        return self._flat_cache
+
+    def _species_n(self):
+        if self.binned:
+            return [0 if b is None else b.n for b in self._bins]
+        return [0 if p is None else p.n for p in self._flat]
 
     def load_host_buffers(self, buffers):
         """Shard full host buffers (reference ParticleBuffers) onto this rank."""
@@ -155,7 +193,7 @@ class DeviceSimulation:
             self.load_species(sid, DeviceParticles.from_host(buf, self.device, start, count))
 
     def total_particles(self):
-        n = sum(p.n for p in self.particles if p is not None)
+        n = sum(self._species_n())
         if self.distributed:
             import torch.distributed as dist
             t = self.torch.tensor([n], dtype=self.torch.int64, device=self.device)
@@ -209,7 +247,7 @@ class DeviceSimulation:
         return ptr
 
     def _fused(self, sid, start, count, stream):
-        p = self.particles[sid]
+        p = self._flat[sid]
         sc = self.scalars[sid]
         L = _lib.load()
         ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
@@ -254,15 +292,21 @@ class DeviceSimulation:
         works = []
         # the cell records are built on `s` before any side stream forks off
         # it (side streams wait on everything queued on `s` so far)
-        self._records_ptr(s)
-        side = self._side_streams(s)
-        for sid, p in enumerate(self.particles):
-            if p is None or p.n == 0:
+        rec = self._records_ptr(s)
+        side = [] if self.binned else self._side_streams(s)
+        self._flat_cache = None
+        for sid, n in enumerate(self._species_n()):
+            if n == 0:
                 continue
             ss = side[sid % len(side)] if side else s
-            for (b0, bn) in partition_batches(p.n, self.batches).spans:
-                if bn:
-                    self._fused(sid, b0, bn, ss)
+            if self.binned:
+                sp = self.species[sid]
+                self._bins[sid].cycle(self._lists, rec, self.acc[sid], self.invvol,
+                                      self.scalars[sid], sp.mover_iters, self.scale, self.status, s)
+            else:
+                for (b0, bn) in partition_batches(n, self.batches).spans:
+                    if bn:
+                        self._fused(sid, b0, bn, ss)
             if reduce and self.distributed:
                 if side:
                     s.wait_stream(ss)
@@ -281,6 +325,8 @@ class DeviceSimulation:
             dist.all_reduce(self.status, op=dist.ReduceOp.MAX, group=self.group)
         ev[3].synchronize()
         st = int(self.status.item())
+        if self.binned:
+            self._bins_after_cycle()
         if st == _lib.ERR_RUNAWAY:
             raise IntegrityError("runaway particle (moved a full box length)")
         if st == _lib.ERR_MIDPOINT:
@@ -288,6 +334,22 @@ class DeviceSimulation:
         if st == _lib.ERR_DOMAIN:
             raise IntegrityError("particle outside the domain at deposition")
         return ev[0].elapsed_time(ev[3]), ev[1].elapsed_time(ev[2])
+
+    def _bins_after_cycle(self):
+        """Overflowed or misplaced particles: re-bin that species (host
+        decision after the synchronised cycle; the moments are complete)."""
+        live = [b for b in self._bins if b is not None]
+        if not live:
+            return
+        stats = self.torch.stack([b.stat for b in live]).cpu().tolist()
+        for b, st in zip(live, stats):
+            b.check_after_cycle(st)
+
+    def bin_stats(self):
+        """Per species: leavers, overflowed, misplaced, lost of the last
+        cycle and the number of rebuilds so far (binned layout)."""
+        return [None if b is None else (b.last_stats or b.stats())[:4] + [b.rebuilds]
+                for b in self._bins]
 
     def fold_moments(self):
         """Phase 4 on device: merge duplicated periodic planes (exact)."""
@@ -352,7 +414,11 @@ class DeviceSimulation:
         return chi
 
     def sort(self):
-        for p in self.particles:
+        """Phase 6.  The binned layout is cell-sorted after every cycle, so
+        only the flat layout sorts."""
+        if self.binned:
+            return
+        for p in self._flat:
             if p is not None:
                 p.sort_by_cell(self.geom)
 
@@ -371,7 +437,8 @@ class DeviceSimulation:
         p3, kt = self.phase3()
         self.fold_moments()
         sort_ms, sorted_now = 0.0, False
-        if self.sort_period > 0 and (self.cycle + 1) % self.sort_period == 0:
+        if (not self.binned and self.sort_period > 0
+                and (self.cycle + 1) % self.sort_period == 0):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             self.sort()

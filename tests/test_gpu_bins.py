@@ -1,0 +1,180 @@
+"""The cell-binned layout of the f32 fast path (bins.py, csrc/bp_bins.cu)
+against the flat layout (the reference's SoA + periodic sort) and the CPU
+oracle.
+
+The binned mover uses the same cell records and the same arithmetic as the
+flat split mover, so particle states must stay BITWISE equal to the flat
+path's, cycle after cycle, whatever happens to the bins (leavers, overflowed
+bins, a full leaver list).  The moments differ only by the f32 summation
+order of the per-bin sums: within the north star's f32 tolerance, written
+here as |bins - flat| <= 1e-5 * max|flat| per moment row."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _gem(cells=(16, 8, 8), box=(6.4, 3.2, 3.2), ppc=12, seed=3, label="single", e_amp=2e-3):
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import GemInit, gem_geometry, gem_species, init_gem_host
+    from paper_2008_04397_b200.gem import smooth_e_field
+    geom = gem_geometry(cells, box)
+    species = gem_species(ppc)
+    prec = PrecisionMode.from_label(label)
+    bufs, fields = init_gem_host(geom, species, GemInit(seed=seed), prec)
+    fields.E[...] = smooth_e_field(geom, e_amp, fields.E.dtype)
+    return geom, species, prec, bufs, fields
+
+
+def _sim(geom, species, prec, bufs, layout, **kw):
+    from paper_2008_04397_b200.pipeline import DeviceSimulation
+    sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith="fast", sort_period=3,
+                           layout=layout, **kw)
+    sim.load_host_buffers([b.copy() for b in bufs])
+    return sim
+
+
+def _by_id(p):
+    h = p.to_host()
+    o = np.argsort(h.ids)
+    return {k: getattr(h, k)[o] for k in ("ids", "x", "y", "z", "u", "v", "w", "q_p")}
+
+
+def _assert_moments_close(a, b, tol=TOL):
+    for x, y in zip(a, b):
+        for r in range(x.shape[0]):
+            ref = x[r].astype(np.float64)
+            err = np.abs(y[r].astype(np.float64) - ref).max() / max(np.abs(ref).max(), 1.0)
+            assert err <= tol, (r, err)
+
+
+def _assert_binned(sim):
+    """Every exported particle lies in the cell of its bin: the export is in
+    bin order, so the f32 cell keys must be non-decreasing."""
+    from paper_2008_04397_b200.kernels import make_geo_arrays
+    geo_f, _ = make_geo_arrays(sim.geom, np.float32)
+    for p in sim.particles:
+        h = p.to_host()
+        g = [np.float32(1.0 / np.float32(sim.geom.spacings[a])) for a in range(3)]
+        o = [np.float32(np.float32(sim.geom.origin[a]) / np.float32(sim.geom.spacings[a]))
+             for a in range(3)]
+        # the kernels' fmaf(x, 1/d, -o/d) in f64 then f32 rounding is the fma
+        gi = [np.minimum(np.trunc((getattr(h, c).astype(np.float64) * g[a] - o[a])
+                                  .astype(np.float32)).astype(np.int64), n - 1)
+              for a, (c, n) in enumerate(zip("xyz", sim.geom.counts))]
+        key = gi[0] + sim.geom.nx * (gi[1] + sim.geom.ny * gi[2])
+        # rounding of the emulated fma can move a particle sitting on a cell
+        # face by one cell; allow no more than that
+        assert np.all(np.diff(key) >= -sim.geom.nx * sim.geom.ny - 1)
+        assert (np.diff(key) < 0).mean() < 1e-3
+
+
+def test_build_export_roundtrip(gpu):
+    geom, species, prec, bufs, fields = _gem()
+    sim = _sim(geom, species, prec, bufs, "bins")
+    assert sim.binned
+    for b, p in zip(bufs, sim.particles):
+        d = _by_id(p)
+        o = np.argsort(b.ids)
+        assert np.array_equal(d["ids"], b.ids[o])
+        for k in "xyzuvw":
+            assert np.array_equal(d[k], getattr(b, k)[o])
+        assert np.array_equal(d["q_p"], b.q_p[o])
+    _assert_binned(sim)
+
+
+@pytest.mark.parametrize("label", ["single", "mixed"])
+def test_bins_match_flat_bitwise_particles(gpu, label):
+    geom, species, prec, bufs, fields = _gem(label=label)
+    a = _sim(geom, species, prec, bufs, "bins")
+    b = _sim(geom, species, prec, bufs, "flat")
+    for cyc in range(6):
+        a.run_cycle(fields.E, fields.B)
+        b.run_cycle(fields.E, fields.B)
+        _assert_moments_close(b.moments_host(), a.moments_host())
+    for pa, pb in zip(a.particles, b.particles):
+        da, db = _by_id(pa), _by_id(pb)
+        for k in da:
+            assert np.array_equal(da[k], db[k]), k
+    st = a.bin_stats()
+    assert all(s[0] > 0 for s in st), st          # particles did change cell
+    assert all(s[1] == 0 and s[3] == 0 for s in st)
+    _assert_binned(a)
+
+
+def test_bins_overflow_and_full_leaver_list(gpu):
+    """No slack at all (every arriving leaver overflows its bin) and a leaver
+    list of a few slots (most leavers stay misplaced): rebuilds every cycle,
+    the particles still bitwise the flat path's, moments within tolerance."""
+    from paper_2008_04397_b200.bins import TransitLists
+    geom, species, prec, bufs, fields = _gem(seed=9)
+    a = _sim(geom, species, prec, bufs, "bins", bin_slack=(0.0, 0))
+    b = _sim(geom, species, prec, bufs, "flat")
+    for cyc in range(4):
+        if cyc == 2:
+            a._lists = TransitLists(a.device, 0)   # 4096 slots: one bin claim's worth
+            a._lists.leaver_cap = 3
+        a.run_cycle(fields.E, fields.B)
+        b.run_cycle(fields.E, fields.B)
+        _assert_moments_close(b.moments_host(), a.moments_host())
+    assert sum(b_.rebuilds for b_ in a._bins) >= 2
+    for pa, pb in zip(a.particles, b.particles):
+        da, db = _by_id(pa), _by_id(pb)
+        for k in da:
+            assert np.array_equal(da[k], db[k]), k
+
+
+def test_bins_against_oracle(gpu, oracle):
+    """One cycle of the binned path against the reference arithmetic (CPU
+    oracle): particles within 1e-4 of max, moments within 1e-4."""
+    from paper_2008_04397_b200 import kernels as K
+    from paper_2008_04397_b200.fields import MOMENT_SCALE
+    geom, species, prec, bufs, fields = _gem(cells=(32, 16, 8), box=(12.8, 6.4, 3.2), ppc=16)
+    a = _sim(geom, species, prec, bufs, "bins")
+    a.run_cycle(fields.E, fields.B)
+    acc_gpu = a.moments_host()
+    geo_f, geo_i = K.make_geo_arrays(geom, np.float32)
+    inv = geom.inv_node_volume(np.float32)
+    for s, b, p, ag in zip(species, bufs, a.particles, acc_gpu):
+        r = b.copy()
+        sc = K.kernel_scalars(s, 0.25, 1.0, np.float32)
+        acc = np.zeros((10,) + geom.node_shape, np.int64)
+        st = oracle.fused_parallel(r.x, r.y, r.z, r.u, r.v, r.w, r.q_p, 0, r.n, fields.E,
+                                   fields.B, acc, inv, geo_f, geo_f, geo_i, sc["dt"], sc["dth"],
+                                   sc["qdt2m"], sc["beta"], sc["one"], 3,
+                                   np.float32(MOMENT_SCALE), 0, os.cpu_count() or 1)
+        assert st == 0
+        oracle_fold = acc.copy()
+        from paper_2008_04397_b200.fields import fold_periodic
+        fold_periodic(oracle_fold, geom)
+        d = _by_id(p)
+        o = np.argsort(r.ids)
+        for k in "xyzuvw":
+            ref = getattr(r, k)[o].astype(np.float64)
+            err = np.abs(d[k] - ref).max() / max(np.abs(ref).max(), 1e-30)
+            assert err <= 1e-4, (k, err)
+        _assert_moments_close([oracle_fold], [ag], tol=1e-4)
+
+
+def test_bins_match_flat_many_per_bin(gpu):
+    """Bins of several 32-particle tiles (ppc 125, as the C3 benchmark):
+    four cycles bitwise against the flat path, no overflow, no misplaced."""
+    geom, species, prec, bufs, fields = _gem(cells=(32, 16, 16), box=(6.4, 3.2, 3.2), ppc=125,
+                                             seed=4, e_amp=1e-4)
+    a = _sim(geom, species, prec, bufs, "bins")
+    b = _sim(geom, species, prec, bufs, "flat")
+    for cyc in range(4):
+        a.run_cycle(fields.E, fields.B)
+        b.run_cycle(fields.E, fields.B)
+        print(cyc, a.bin_stats())
+        assert all(s[1] == 0 and s[2] == 0 and s[3] == 0 for s in a.bin_stats()), a.bin_stats()
+        _assert_moments_close(b.moments_host(), a.moments_host())
+    for pa, pb in zip(a.particles, b.particles):
+        da, db = _by_id(pa), _by_id(pb)
+        for k in da:
+            assert np.array_equal(da[k], db[k]), k
