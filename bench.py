@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--precision", default="single", choices=("single", "mixed", "double"))
     ap.add_argument("--arith", default="fast", choices=("fast", "parity"))
     ap.add_argument("--sort-period", type=int, default=10)
+    ap.add_argument("--layout", default="auto", choices=("auto", "flat", "bins"),
+                    help="particle layout of the device path (pipeline.DeviceSimulation)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -85,7 +87,8 @@ def workload_config(args, world):
         "workload": f"gem{dim}_{cells[0]}x{cells[1]}x{cells[2]}_ppc{args.ppc}x4",
         "cells": list(cells), "particles": n, "species": 4, "ppc": args.ppc,
         "precision": args.precision, "arith": args.arith, "mover_iters": 3, "dt": 0.25,
-        "sort_period": args.sort_period, "decomposition": f"particles/{world} ranks",
+        "sort_period": args.sort_period, "layout": args.layout,
+        "decomposition": f"particles/{world} ranks",
         "l2_flush": f"none: {traffic:.1f} GB of particle traffic per step >> 126 MB L2",
     }
 
@@ -263,7 +266,9 @@ def main_ours(args):
     species = gem_species(args.ppc)
     prec = PrecisionMode.from_label(args.precision)
     sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=args.arith,
-                           sort_period=args.sort_period, device=dev, distributed=world > 1)
+                           sort_period=args.sort_period, device=dev, distributed=world > 1,
+                           layout=args.layout)
+    config["layout"] = "bins" if sim.binned else "flat"
     c0, nc = shard_span(geom.n_cells, rank, world)
     for sid, p in enumerate(init_gem_device(geom, species, dev, precision=prec, cells=(c0, nc))):
         sim.load_species(sid, p)
@@ -335,6 +340,9 @@ def main_ours(args):
     names = {"mover": "bp::sk::mover_kernel (implicit mover, 3 iterations)",
              "deposit": "bp::sk::deposit_kernel (10-moment interpolation)",
              "span": "bp::span_kernel (generic fused mover + deposit)"}
+    if sim.binned:
+        names.update(mover="bp::bins::mover_bins (implicit mover on cell bins, 3 iterations)",
+                     deposit="bp::bins::deposit_bins (10-moment interpolation on cell bins)")
     traffic = ncu_traffic(dom) if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
                                    and args.precision == "single"
                                    and args.arith == "fast") else None
@@ -355,13 +363,27 @@ def main_ours(args):
     extra = {"phase3_kernel_ms_per_step": kern_ms / args.steps,
              "sort_ms_per_sort": sort_ms / max(1, sum(t.sorted_this_cycle for t in timed)),
              "phase3_particles_per_s": n_total / (kern_ms / args.steps * 1e-3)}
+    if sim.binned:
+        # per species, last timed cycle: leavers, overflowed, misplaced, lost,
+        # rebuilds so far
+        extra["bin_stats"] = sim.bin_stats()
 
     # bitwise reference arithmetic beside it
     if not args.no_parity and args.arith != "parity":
-        sim._arith = _lib.ARITH_PARITY
+        # the bitwise arithmetic runs on the flat layout: a second simulation
+        # over this one's particles (exported in cell order)
+        psim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith="parity",
+                                sort_period=args.sort_period, device=dev,
+                                distributed=world > 1, layout="flat")
+        for sid, p in enumerate(sim.particles):
+            psim.load_species(sid, p)
+        psim.set_fields(f.E, f.B)
+
+        def pstep(timing):
+            timing.append(psim.run_cycle())
         pt = []
         for _ in range(2):
-            step(pt)
+            pstep(pt)
         pt = []
         barrier()
         torch.cuda.synchronize()
@@ -369,7 +391,7 @@ def main_ours(args):
         ks = max(2, min(args.steps, 5))
         p0.record()
         for _ in range(ks):
-            step(pt)
+            pstep(pt)
         p1.record()
         torch.cuda.synchronize()
         pe = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
@@ -377,7 +399,8 @@ def main_ours(args):
             dist.all_reduce(pe, op=dist.ReduceOp.MAX)
         extra["parity_arith"] = {"value": n_total * ks / (float(pe) * 1e-3), "unit": UNIT,
                                  "steps": ks, "note": "bitwise-reference arithmetic"}
-        sim._arith = _lib.ARITH_FAST if args.arith == "fast" else _lib.ARITH_PARITY
+        del psim, pt
+        torch.cuda.empty_cache()
 
     # end to end through the host-buffer C ABI (pinned host particles)
     e2e = None
