@@ -41,3 +41,24 @@ def test_kernel_objects_are_sm100a():
     out = subprocess.run([exe, "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def _param_counts():
+    """Parameter count of every declaration in include/bp_b200.h."""
+    text = open(os.path.join(ROOT, "include", "bp_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"^\s*(?:int|int64_t|long long|const char\*)\s+(bp_\w+)\s*\(([^)]*)\)\s*;",
+                         text, re.M):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_header():
+    # a wrong argtypes length silently shifts every later argument
+    from paper_2008_04397_b200 import _lib
+    counts = _param_counts()
+    assert set(counts) == set(_lib.EXPORTS)
+    for name, (_res, argtypes) in _lib._SIGS.items():
+        assert len(argtypes) == counts[name], (name, len(argtypes), counts[name])
