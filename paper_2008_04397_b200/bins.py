@@ -32,7 +32,7 @@ def _ptr(t):
 class BinnedSpecies:
     """One species' particles in per-cell bins on one device."""
 
-    def __init__(self, parts, geom, geo_f, geo_g, geo_i, fbytes, slack=(0.5, 32),
+    def __init__(self, parts, geom, geo_f, geo_g, geo_i, fbytes, slack=(0.5, 64),
                  overflow_frac=1.0 / 16, stream=None):
         import torch
         if parts.dtype != torch.float32:
@@ -81,16 +81,25 @@ class BinnedSpecies:
         if rc == _lib.ERR_DOMAIN:
             raise DomainError("positions below the box origin")
         cap = int(total.value)
-        dev = self.device
         self.cap = cap
-        self.arrs = [torch.empty(max(cap, 1), dtype=torch.float32, device=dev) for _ in ARRAYS]
-        self.ids = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        self.arrs, self.ids = self._alloc_set(cap)
+        # the re-slack's destination, allocated now: a re-slack inside a run
+        # then only copies (no multi-GB allocation in the middle of a cycle)
+        self._spare = self._alloc_set(cap)
         dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in self.arrs])
         rc = L.bp_bins_fill(self.fbytes, *[_ptr(a) for a in parts.arrays()], _ptr(parts.ids),
                             parts.n, gf, gg, gi, _ptr(self.start), dst, _ptr(self.ids),
                             ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_fill")
         self.n = parts.n
+
+    def _alloc_set(self, cap):
+        """One buffer set (x..q, ids) for `cap` slots plus headroom (3% + 64k
+        slots), so that the slightly larger layouts of later re-slacks fit."""
+        torch = self.torch
+        n = int(cap * 1.03) + (1 << 16)
+        return ([torch.empty(n, dtype=torch.float32, device=self.device) for _ in ARRAYS],
+                torch.empty(n, dtype=torch.int64, device=self.device))
 
     def flat(self, stream=None):
         """The live particles (bins in cell order, then the overflow list of
@@ -142,11 +151,9 @@ class BinnedSpecies:
                                ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_reslack")
         cap = int(total.value)
-        spare = getattr(self, "_spare", None)
-        if spare is None or spare[1].numel() < cap:
-            spare = ([torch.empty(max(cap, 1), dtype=torch.float32, device=self.device)
-                      for _ in ARRAYS],
-                     torch.empty(max(cap, 1), dtype=torch.int64, device=self.device))
+        spare = self._spare
+        if spare[1].numel() < cap:
+            spare = self._alloc_set(cap)
         dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in spare[0]])
         rc = L.bp_bins_reslack(*args, dst, _ptr(spare[1]), ctypes.byref(total),
                                ctypes.c_void_p(s.cuda_stream))

@@ -86,18 +86,7 @@ struct Bins {
   Leaver* late;  // the deposit's misplaced particles (deposited by deposit_list)
   long long late_cap;
   unsigned long long* stat;  // [ST_N]
-  int variant;  // measurement knobs (BP_BINS_VARIANT), 0 = default
 };
-
-// particle stream loads / stores by variant: 0 streaming (.cs), 1 read-only
-// path (.nc), 2 default caching
-__device__ __forceinline__ float ld_p(const float* p, int v) {
-  return v == 0 ? __ldcs(p) : (v == 1 ? __ldg(p) : *p);
-}
-__device__ __forceinline__ void st_p(float* p, float x, int v) {
-  if (v == 0) __stcs(p, x);
-  else *p = x;
-}
 
 constexpr int kHoleCap = 64;     // leavers per bin per cycle tracked for the refill
 constexpr int kMoveClaim = 8;    // bins per mover work claim
@@ -292,11 +281,11 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
   int c0 = claim(0);
   // prefetched particle (one per lane) and the slot it came from
   float n1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const int lv_ = b.variant & 3, sv_ = (b.variant >> 2) & 1;
   auto fetch = [&](long long q, bool ok) {
     if (ok) {
-      n1[0] = ld_p(b.x + q, lv_); n1[1] = ld_p(b.y + q, lv_); n1[2] = ld_p(b.z + q, lv_);
-      n1[3] = ld_p(b.u + q, lv_); n1[4] = ld_p(b.v + q, lv_); n1[5] = ld_p(b.w + q, lv_);
+      // streaming loads (read once per cycle)
+      n1[0] = __ldcs(b.x + q); n1[1] = __ldcs(b.y + q); n1[2] = __ldcs(b.z + q);
+      n1[3] = __ldcs(b.u + q); n1[4] = __ldcs(b.v + q); n1[5] = __ldcs(b.w + q);
     }
   };
   float4 R[12];
@@ -408,8 +397,8 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
         // written; write-back stores, so the refill and the migration find
         // the bin's lines in L2
         if (valid && st == ST_OK) {
-          st_p(b.x + p, xp, sv_); st_p(b.y + p, yp, sv_); st_p(b.z + p, zp, sv_);
-          st_p(b.u + p, un, sv_); st_p(b.v + p, vn, sv_); st_p(b.w + p, wn, sv_);
+          __stcs(b.x + p, xp); __stcs(b.y + p, yp); __stcs(b.z + p, zp);
+          __stcs(b.u + p, un); __stcs(b.v + p, vn); __stcs(b.w + p, wn);
         }
       }
         __syncwarp();
@@ -559,12 +548,12 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
   const float* const rd = ws + (8 * qd) * kRowS + 8 * qd + l;
   const int ci_off = l & 1, cj_off = (l >> 1) & 1, ck_off = (l >> 2) & 1;
   float n1[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const int dv_ = 1 + ((b.variant >> 4) & 1);  // read-only path by default (measured)
   auto fetch = [&](long long q, bool ok) {
     if (ok) {
-      n1[0] = ld_p(b.x + q, dv_); n1[1] = ld_p(b.y + q, dv_); n1[2] = ld_p(b.z + q, dv_);
-      n1[3] = ld_p(b.u + q, dv_); n1[4] = ld_p(b.v + q, dv_); n1[5] = ld_p(b.w + q, dv_);
-      n1[6] = ld_p(b.q + q, dv_);
+      // read-only path (measured faster than streaming loads here)
+      n1[0] = __ldg(b.x + q); n1[1] = __ldg(b.y + q); n1[2] = __ldg(b.z + q);
+      n1[3] = __ldg(b.u + q); n1[4] = __ldg(b.v + q); n1[5] = __ldg(b.w + q);
+      n1[6] = __ldg(b.q + q);
     }
   };
   for (;;) {
@@ -920,11 +909,6 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   b.late = (bins::Leaver*)ba.late;
   b.late_cap = ba.late_cap;
   b.stat = (unsigned long long*)ba.stat;
-  static const int variant = [] {
-    const char* e = getenv("BP_BINS_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  b.variant = variant;
   cudaMemsetAsync(b.stat, 0, bins::ST_N * sizeof(unsigned long long), s);
   int rc = launch_mover_bins_any(a, b, c.geo_i, s);
   if (rc) return rc;

@@ -100,7 +100,11 @@ class DeviceSimulation:
     # cycles) or "bins" (per-cell bins kept sorted every cycle, bins.py; f32
     # particles with the fast arithmetic); "auto" picks bins where they apply
     layout: str = "auto"
-    bin_slack: tuple = (0.5, 32)
+    # bin capacity = count + max(slack[1], slack[0] * count), rounded to 8
+    # slots: a bin that fills up forces a re-slack of the species (a copy of
+    # all bins); 64 slots of minimum headroom keep that to every ~10 cycles at
+    # C3 (bins near the sheet fill by ~5 particles per cycle)
+    bin_slack: tuple = (0.5, 64)
 
     def __post_init__(self):
         import torch
