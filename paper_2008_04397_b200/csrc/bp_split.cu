@@ -252,6 +252,7 @@ __device__ __forceinline__ void patch_flush(const Params<T>& a, T* patch,
       }
     }
   }
+  __syncwarp();  // the cleared patch is written by the other lanes' folds next
 }
 
 // main fold of all 32 staged particles for this lane's three values: rows of
@@ -431,6 +432,9 @@ __global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constan
         const int kg = __shfl_sync(0xffffffffu, pnode, __ffs(rest) - 1);
         const unsigned MG = __ballot_sync(0xffffffffu, fit && pnode == kg);
         rest &= ~MG;
+        // a neighbouring lane may have written this node (its corner of the
+        // previous group's cell): order the patch accesses of the warp
+        __syncwarp();
         // the cell's patch values are read first (no alias with the staged
         // rows) so their latency hides behind the fold
         const T o0 = pv0[kg], o1 = pv1[kg], o2 = pv2[kg];
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constan
                     (unsigned long long)lattice(a, t2s, node));
       }
       if (V & ~Mm) {
+        __syncwarp();  // every lane is done reading the staged rows
         if (((V & ~Mm) >> lane) & 1u) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) st_bs[c * KR + lane] = T(0);
