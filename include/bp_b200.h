@@ -271,6 +271,30 @@ int bp_bins_export(float* const* src, int64_t* ids, const int64_t* start, int32_
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream);
 
+/* ------------------------------------------------------------------------
+ * Bit-exact device loader: one species of the reference's init_maxwellian
+ * (pkg/src/batchpic/particles.py:177-241, _species_rng :173-175) generated in
+ * HBM for the cells [c0, c0 + nc) (x fastest, ppc particles each: the rank's
+ * shard).  Positions o + d (cell index) + d U and velocities drift + vth N
+ * with U / N numpy's Generator(Philox(key=[seed, species_id])).random /
+ * .standard_normal draws (jitter (3, n_p) first, normals (3, n_p) next),
+ * cast to the particle dtype (pbytes); q = q_cell[cell - c0] (the caller's
+ * species.charge * density(cell centre) * cell volume / ppc); ids = the
+ * global particle index.  All outputs, q_cell, tail_k / tail_u: DEVICE;
+ * geo_i, origin[3], spacing[3], drift[3], vth[3], n_tail: host.  Normals of
+ * the ziggurat's tail strip (~0.03%) are bit-exact only with the host libm's
+ * log1p: each is listed as tail_k = 2 * ordinal + sign, tail_u = its
+ * uniform, and the caller finishes it as +-(r - log1p(-u) / r)
+ * (numpy random_standard_normal; paper_2008_04397_b200/gem.py does).
+ * Synchronises; *n_tail = listed tail normals (> tail_cap: error).
+ */
+int bp_init_maxwellian(int pbytes, uint64_t seed, uint64_t species_id, const int64_t* geo_i,
+                       const double* origin, const double* spacing, int ppc,
+                       const double* drift, const double* vth, const double* q_cell,
+                       int64_t c0, int64_t nc, void* xs, void* ys, void* zs, void* us,
+                       void* vs, void* ws, void* qs, int64_t* ids, int64_t* tail_k,
+                       double* tail_u, int64_t tail_cap, int64_t* n_tail, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,7 @@ EXPORTS = (
     "bp_field_records_bytes", "bp_field_records_build", "bp_fused_span_rec",
     "bp_timing_enable", "bp_timing_read",
     "bp_bins_leaver_bytes", "bp_bins_plan", "bp_bins_fill", "bp_bins_cycle", "bp_bins_export",
-    "bp_bins_reslack",
+    "bp_bins_reslack", "bp_init_maxwellian",
 )
 
 _P = ctypes.c_void_p
@@ -76,6 +76,8 @@ _SIGS = {
     "bp_bins_cycle": (_INT, [_INT] + [_P] * 10 + [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,
                                                    _P, _P]
                       + [_P, _P, _P] + [_D] * 5 + [_INT, _D, _P, _P]),
+    "bp_init_maxwellian": (_INT, [_INT, ctypes.c_uint64, ctypes.c_uint64] + [_P] * 3
+                           + [_INT] + [_P] * 3 + [_I64, _I64] + [_P] * 10 + [_I64, _P, _P]),
     "bp_bins_export": (_INT, [_P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "bp_bins_reslack": (_INT, [_P, _P, _P, _P, _I64, _P, _I64, _P, _D, _INT, _P, _P, _P, _P, _P,
                                _P]),

@@ -786,3 +786,51 @@ int bp_bins_reslack(float* const* src, int64_t* ids, const int64_t* start, int32
   return bins_reslack_copy(ba, (void* const*)src, new_start, new_count, dst, dst_ids,
                            (cudaStream_t)stream);
 }
+
+// ---------------------------------------------------------------------------
+// Bit-exact device loader (bp_init.cu)
+int bp_init_maxwellian(int pbytes, uint64_t seed, uint64_t species_id, const int64_t* geo_i,
+                       const double* origin, const double* spacing, int ppc,
+                       const double* drift, const double* vth, const double* q_cell,
+                       int64_t c0, int64_t nc, void* xs, void* ys, void* zs, void* us,
+                       void* vs, void* ws, void* qs, int64_t* ids, int64_t* tail_k,
+                       double* tail_u, int64_t tail_cap, int64_t* n_tail, void* stream) {
+  if ((pbytes != 4 && pbytes != 8) || !geo_i || !origin || !spacing || !drift || !vth ||
+      !q_cell || ppc < 1 || c0 < 0 || nc < 0 || !xs || !ys || !zs || !us || !vs || !ws ||
+      !qs || !ids || !n_tail || tail_cap < 0 || (tail_cap > 0 && (!tail_k || !tail_u))) {
+    set_error("init_maxwellian: bad arguments");
+    return BP_EINVAL;
+  }
+  const int64_t n_cells = geo_i[0] * geo_i[1] * geo_i[2];
+  if (n_cells <= 0 || c0 + nc > n_cells || n_cells * (int64_t)ppc > ((int64_t)1 << 40)) {
+    set_error("init_maxwellian: cell range outside the grid");
+    return BP_EINVAL;
+  }
+  ensure_pool();
+  InitArgs A{};
+  A.pbytes = pbytes;
+  A.seed = seed;
+  A.species_id = species_id;
+  A.n_cells = n_cells;
+  A.nx = geo_i[0];
+  A.ny = geo_i[1];
+  A.ppc = ppc;
+  A.c0 = c0;
+  A.nc = nc;
+  for (int a = 0; a < 3; ++a) {
+    A.origin[a] = origin[a];
+    A.spacing[a] = spacing[a];
+    A.drift[a] = drift[a];
+    A.vth[a] = vth[a];
+  }
+  A.q_cell = q_cell;
+  void* arr[7] = {xs, ys, zs, us, vs, ws, qs};
+  for (int k = 0; k < 7; ++k) A.arr[k] = arr[k];
+  A.ids = ids;
+  A.tail_k = tail_k;
+  A.tail_u = tail_u;
+  A.tail_cap = tail_cap;
+  A.n_tail = n_tail;
+  *n_tail = 0;
+  return init_maxwellian(A, (cudaStream_t)stream);
+}

@@ -71,6 +71,26 @@ int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t
 int bins_reslack_copy(const BinsArgs& ba, void* const* src, const int64_t* nstart, int* ncount,
                       void* const* dst, int64_t* dst_ids, cudaStream_t s);
 
+// Bit-exact device loader (bp_init.cu): one species of the reference's
+// init_maxwellian on the cell range [c0, c0 + nc)
+struct InitArgs {
+  int pbytes;
+  uint64_t seed, species_id;
+  int64_t n_cells, nx, ny;
+  int ppc;
+  int64_t c0, nc;
+  double origin[3], spacing[3], drift[3], vth[3];
+  const double* q_cell;  // [nc] device
+  void* arr[7];          // x y z u v w q (device, nc * ppc each)
+  int64_t* ids;
+  int64_t* tail_k;       // tail-strip normals: 2 * ordinal + sign
+  double* tail_u;        // ... and the accepted uniform
+  int64_t tail_cap;
+  int64_t* n_tail;       // host
+  int skip_velocities;
+};
+int init_maxwellian(const InitArgs& A, cudaStream_t s);
+
 // count of kernels this library launched (bp_kernel_launches)
 void note_launch(int n = 1);
 

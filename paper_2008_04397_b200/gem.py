@@ -2,11 +2,10 @@
 Harris sheet with flux perturbation, two current-carrying and two background
 species.
 
-``init_gem_host`` reproduces the reference loader bit for bit (same numpy
-Philox streams and expression order) for parity runs;
-``init_gem_device`` draws the same distributions directly in HBM with torch's
-device RNG (synthetic GEM-shaped data for benchmarks of 1e8-1e9 particles,
-not bit-identical to the host loader).
+``init_gem_host`` reproduces the reference loader bit for bit on the host
+(same numpy Philox streams and expression order); ``init_gem_device``
+generates the same buffers bit for bit directly in HBM (csrc/bp_init.cu), the
+loader of the device-resident runs and benchmarks (1e8-1e9 particles).
 """
 
 from __future__ import annotations
@@ -136,50 +135,36 @@ def init_gem_host(geom, species, init=GemInit(), precision=None, c=1.0):
 
 def init_gem_device(geom, species, device, init=GemInit(), precision=None, c=1.0,
                     cells=None, id_offset=0):
-    """GEM-shaped particles generated in HBM: cell-major (already sorted),
-    ppc per cell, uniform jitter, drifting Maxwellian velocities, charge
-    weights from the sheet / background density at the cell centre — the
-    reference loader's distributions, drawn with torch's device Philox.
+    """The reference loader (gem.py:64-115 -> particles.py:177-241) generated
+    in HBM, bit-identical to it (particles.init_maxwellian_device: the same
+    Philox(seed, species) draws, ziggurat normals, expression order; sheet /
+    background densities at the cell centres).
 
     ``cells`` = (first, count) restricts the load to a contiguous range of
-    cells (x-fastest order), which is how ranks get their particle shard."""
-    import torch
+    cells (x-fastest order), which is how ranks get their particle shard;
+    ``id_offset`` is added to the (global) particle ids."""
+    from .particles import init_maxwellian_device
     _check(species)
-    mode = precision or PrecisionMode()
-    pdt = torch.float32 if mode.particle_dtype == np.float32 else torch.float64
-    c0, nc = (0, geom.n_cells) if cells is None else cells
     yc = geom.origin[1] + 0.5 * geom.Ly
     lam = init.sheet_thickness
     u_e, u_i = sheet_drifts(species, init, c)
-    drift_z = {SHEET_ELECTRON: u_e, SHEET_ION: u_i, BG_ELECTRON: 0.0, BG_ION: 0.0}
+
+    def sheet(x, y, z):
+        return init.n0 / np.cosh((y - yc) / lam) ** 2
+
+    def bg(x, y, z):
+        return np.full_like(np.asarray(y, dtype=np.float64), init.background_fraction * init.n0)
+
+    drifts = {SHEET_ELECTRON: (0.0, 0.0, u_e), SHEET_ION: (0.0, 0.0, u_i),
+              BG_ELECTRON: (0.0, 0.0, 0.0), BG_ION: (0.0, 0.0, 0.0)}
     out = []
     for s in species:
-        g = torch.Generator(device=device)
-        g.manual_seed(init.seed * 1_000_003 + s.species_id * 7919 + c0)
-        ppc = s.ppc
-        n = nc * ppc
-        lin = torch.arange(c0, c0 + nc, device=device, dtype=torch.int64)
-        ci, cj, ck = lin % geom.nx, (lin // geom.nx) % geom.ny, lin // (geom.nx * geom.ny)
-        arrs = []
-        for a, cidx in enumerate((ci, cj, ck)):
-            d, o = geom.spacings[a], geom.origin[a]
-            jit = torch.rand(n, device=device, dtype=torch.float64, generator=g)
-            arrs.append((o + d * cidx.repeat_interleave(ppc).to(torch.float64) + d * jit).to(pdt))
-        for a in range(3):
-            dv = drift_z[s.species_id] if a == 2 else 0.0
-            nrm = torch.randn(n, device=device, dtype=torch.float64, generator=g)
-            arrs.append((dv + s.vth[a] * nrm).to(pdt))
-        ycell = geom.origin[1] + geom.dy * (cj.to(torch.float64) + 0.5)
-        if s.species_id < 2:
-            dens = init.n0 / torch.cosh((ycell - yc) / lam) ** 2
-        else:
-            dens = torch.full_like(ycell, init.background_fraction * init.n0)
-        q = (s.charge * dens * geom.cell_volume / ppc).repeat_interleave(ppc)
-        arrs.append(q.to(pdt))
-        ids = torch.arange(id_offset + c0 * ppc, id_offset + (c0 + nc) * ppc, device=device,
-                           dtype=torch.int64)
-        out.append(DeviceParticles(*arrs, ids, species_id=s.species_id))
-        del lin, ci, cj, ck
+        p = init_maxwellian_device(s, geom, device, density_fn=sheet if s.species_id < 2 else bg,
+                                   seed=init.seed, precision=precision,
+                                   drift=drifts[s.species_id], cells=cells)
+        if id_offset:
+            p.ids += id_offset
+        out.append(p)
     return out
 
 
@@ -220,31 +205,13 @@ def sample_host(geom, species, cells, init=GemInit(), precision=None, c=1.0, see
 
 
 def init_uniform_device(geom, species, device, n0=1.0, precision=None, cells=None, seed=1):
-    """Uniform drifting-Maxwellian plasma in HBM (the reference's
-    ``init.kind = uniform`` loader, pipeline.py:140-151, with torch's device
-    RNG): ppc particles per cell, cell-major, charge weight
-    q * n0 * V_cell / ppc."""
-    import torch
-    mode = precision or PrecisionMode()
-    pdt = torch.float32 if mode.particle_dtype == np.float32 else torch.float64
-    c0, nc = (0, geom.n_cells) if cells is None else cells
-    out = []
-    for s in species:
-        g = torch.Generator(device=device)
-        g.manual_seed(seed * 1_000_003 + s.species_id * 7919 + c0)
-        n = nc * s.ppc
-        lin = torch.arange(c0, c0 + nc, device=device, dtype=torch.int64)
-        idx = (lin % geom.nx, (lin // geom.nx) % geom.ny, lin // (geom.nx * geom.ny))
-        arrs = []
-        for a, cidx in enumerate(idx):
-            d, o = geom.spacings[a], geom.origin[a]
-            jit = torch.rand(n, device=device, dtype=torch.float64, generator=g)
-            arrs.append((o + d * cidx.repeat_interleave(s.ppc).to(torch.float64) + d * jit).to(pdt))
-        for a in range(3):
-            nrm = torch.randn(n, device=device, dtype=torch.float64, generator=g)
-            arrs.append((s.drift[a] + s.vth[a] * nrm).to(pdt))
-        arrs.append(torch.full((n,), s.charge * n0 * geom.cell_volume / s.ppc, device=device,
-                               dtype=pdt))
-        ids = torch.arange(c0 * s.ppc, (c0 + nc) * s.ppc, device=device, dtype=torch.int64)
-        out.append(DeviceParticles(*arrs, ids, species_id=s.species_id))
-    return out
+    """The reference's uniform loader (make_state for init.kind != "gem",
+    pipeline.py:140-151: init_maxwellian with density n0) generated in HBM,
+    bit-identical to it (particles.init_maxwellian_device)."""
+    from .particles import init_maxwellian_device
+
+    def uniform(x, y, z):
+        return np.full_like(np.asarray(y, dtype=np.float64), n0)
+
+    return [init_maxwellian_device(s, geom, device, density_fn=uniform, seed=seed,
+                                   precision=precision, cells=cells) for s in species]

@@ -149,6 +149,88 @@ def _species_rng(seed, species_id):
     return np.random.Generator(np.random.Philox(key=key))
 
 
+def cell_charges(species, geom, density_fn=None):
+    """Per-cell charge weight q n(cell centre) V_cell / ppc over all cells,
+    x fastest (particles.py:222-230, the same array expressions)."""
+    nc = geom.n_cells
+    lin = np.arange(nc)
+    ci = lin % geom.nx
+    cj = (lin // geom.nx) % geom.ny
+    ck = lin // (geom.nx * geom.ny)
+    if density_fn is None:
+        dens = np.ones(nc)
+    else:
+        cx, cy, cz = (geom.cell_centers(a) for a in range(3))
+        dens = np.asarray(density_fn(cx[ci], cy[cj], cz[ck]), dtype=np.float64)
+        if (dens <= 0.0).any():
+            raise ConfigurationError("density profile must be positive")
+    return species.charge * dens * geom.cell_volume / species.ppc
+
+
+# numpy random_standard_normal's tail strip (distributions.c): r and 1/r
+_ZIG_R, _ZIG_INV_R = 3.6541528853610087963519472518, 0.27366123732975827203338247596
+
+
+def init_maxwellian_device(species, geom, device, density_fn=None, seed=1, precision=None,
+                           drift=None, cells=None):
+    """init_maxwellian generated in HBM (csrc/bp_init.cu, bp_init_maxwellian):
+    the same Philox(key=[seed, species]) draws, cell-major order and
+    arithmetic, so the buffers are bit-identical to the reference's
+    (particles.py:177-241).  ``cells`` = (first, count) loads only that
+    contiguous cell range (a rank's shard; ids stay the global indices).
+    The ziggurat's tail-strip normals (~0.03%) are finished here with the host
+    libm's log1p, as numpy computes them."""
+    import ctypes
+    import math
+    import torch
+    from . import _lib
+    mode = precision or PrecisionMode()
+    pd = mode.particle_dtype
+    tdt = torch.float32 if pd == np.float32 else torch.float64
+    ppc = species.ppc
+    c0, nc = (0, geom.n_cells) if cells is None else (int(cells[0]), int(cells[1]))
+    n = nc * ppc
+    n_p = geom.n_cells * ppc
+    q_cell = torch.from_numpy(
+        np.ascontiguousarray(cell_charges(species, geom, density_fn)[c0:c0 + nc])).to(device)
+    arrs = [torch.empty(n, dtype=tdt, device=device) for _ in ARRAYS]
+    ids = torch.empty(n, dtype=torch.int64, device=device)
+    dv = species.drift if drift is None else tuple(drift)
+    cap = max(4096, (3 * n) // 1000)
+    tk = torch.empty(cap, dtype=torch.int64, device=device)
+    tu = torch.empty(cap, dtype=torch.float64, device=device)
+    ntail = ctypes.c_int64(0)
+    d3 = lambda v: (ctypes.c_double * 3)(*[float(x) for x in v])  # noqa: E731
+    geo_i = (ctypes.c_int64 * 3)(geom.nx, geom.ny, geom.nz)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    L = _lib.load()
+    rc = L.bp_init_maxwellian(
+        np.dtype(pd).itemsize, int(seed), int(species.species_id), geo_i, d3(geom.origin),
+        d3(geom.spacings), ppc, d3(dv), d3(species.vth), ptr(q_cell), c0, nc,
+        *[ptr(a) for a in arrs], ptr(ids), ptr(tk), ptr(tu), cap, ctypes.byref(ntail),
+        ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+    _lib.check(rc, "init_maxwellian")
+    nt = int(ntail.value)
+    if nt > cap:
+        raise IntegrityError(f"init_maxwellian: {nt} tail normals exceed the list ({cap})")
+    if nt:
+        ks, us = tk[:nt].cpu().numpy(), tu[:nt].cpu().numpy()
+        per = [([], []) for _ in range(3)]
+        for kk, u in zip(ks.tolist(), us.tolist()):
+            k, neg = kk >> 1, kk & 1
+            xx = -_ZIG_INV_R * math.log1p(-u)
+            val = -(_ZIG_R + xx) if neg else _ZIG_R + xx
+            a, p = divmod(k, n_p)
+            per[a][0].append(p - c0 * ppc)
+            per[a][1].append(dv[a] + species.vth[a] * val)
+        for a in range(3):
+            if per[a][0]:
+                idx = torch.tensor(per[a][0], dtype=torch.int64, device=device)
+                val = torch.from_numpy(np.asarray(per[a][1], np.float64).astype(pd)).to(device)
+                arrs[3 + a].index_copy_(0, idx, val)
+    return DeviceParticles(*arrs, ids, species_id=species.species_id)
+
+
 def init_maxwellian(species, geom, density_fn=None, seed=1, precision=None, drift=None):
     """Cell-major loading of ``ppc`` particles per cell, drifting Maxwellian
     velocities, charge weights from the density at cell centres — the same
@@ -174,14 +256,7 @@ def init_maxwellian(species, geom, density_fn=None, seed=1, precision=None, drif
     dv = species.drift if drift is None else tuple(drift)
     nrm = rng.standard_normal((3, n_p))
     vel = [dv[a] + species.vth[a] * nrm[a] for a in range(3)]
-    if density_fn is None:
-        dens = np.ones(nc)
-    else:
-        cx, cy, cz = (geom.cell_centers(a) for a in range(3))
-        dens = np.asarray(density_fn(cx[ci], cy[cj], cz[ck]), dtype=np.float64)
-        if (dens <= 0.0).any():
-            raise ConfigurationError("density profile must be positive")
-    q_p = np.repeat(species.charge * dens * geom.cell_volume / ppc, ppc)
+    q_p = np.repeat(cell_charges(species, geom, density_fn), ppc)
     buf = ParticleBuffer(*(a.astype(pd) for a in pos + vel + [q_p]),
                          ids=np.arange(n_p, dtype=np.int64), species_id=species.species_id)
     return buf.validate(geom)
