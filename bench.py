@@ -75,6 +75,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-shuffled", action="store_true")
     return ap.parse_args()
 
 
@@ -103,9 +104,9 @@ def peaks():
 
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
-    summary (profiles/ncu_summary_r01.json), or None."""
+    summary (profiles/ncu_summary_r02.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary_r02.json")) as f:
             return float(json.load(f)[kernel]["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -343,7 +344,7 @@ def main_ours(args):
     if sim.binned:
         names.update(mover="bp::bins::mover_bins (implicit mover on cell bins, 3 iterations)",
                      deposit="bp::bins::deposit_bins (10-moment interpolation on cell bins)")
-    traffic = ncu_traffic(dom) if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
+    traffic = ncu_traffic(dom + ("_bins" if sim.binned else "")) if (world == 1 and cells == (128, 64, 64) and args.ppc == 125
                                    and args.precision == "single"
                                    and args.arith == "fast") else None
     roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": hbm, "unit": "GB/s",
@@ -402,6 +403,12 @@ def main_ours(args):
         del psim, pt
         torch.cuda.empty_cache()
 
+    # unsorted worst case: the flat layout with every species randomly
+    # permuted and no sort (each particle's cell record and deposit target is
+    # a random cell: L2 instead of L1 reuse)
+    if not args.no_shuffled and args.precision != "double":
+        extra["shuffled"] = shuffled_leg(args, sim, geom, species, prec, f, dist, dev, n_total)
+
     # end to end through the host-buffer C ABI (pinned host particles)
     e2e = None
     if not args.no_e2e:
@@ -413,6 +420,10 @@ def main_ours(args):
         cores = os.cpu_count() or 1
         rate, desc = cpu_fused_rate(geom, species, prec, args.cpu_seconds, cores)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+        r1, d1 = cpu_fused_rate(geom, species, prec, max(2.0, args.cpu_seconds / 3), 1,
+                                cells_hint=256)
+        extra["cpu_1thread"] = {"value": r1, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": d1}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -420,12 +431,49 @@ def main_ours(args):
                "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None,
                "dtype": "f32" if args.precision != "double" else "f64",
-               "data": "synthetic (GEM-shaped particles drawn in HBM, Harris+perturbation B)",
+               "data": "synthetic: the reference GEM loader's particles (Philox seed 20250809, "
+                       "generated bit-exactly in HBM by gem.init_gem_device), Harris + "
+                       "perturbation B, smooth E",
                "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "clocks": mon.summary(), "extra": extra}
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def shuffled_leg(args, sim, geom, species, prec, fields, dist, dev, n_total):
+    """Fused phase on randomly permuted particles (flat layout, no sort):
+    device time of a few cycles, max over ranks."""
+    import torch
+    from paper_2008_04397_b200.pipeline import DeviceSimulation
+    from paper_2008_04397_b200.particles import DeviceParticles
+    ssim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=args.arith,
+                            sort_period=0, device=dev, distributed=dist is not None,
+                            layout="flat")
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    for sid, p in enumerate(sim.particles):
+        perm = torch.randperm(p.n, device=dev, generator=g)
+        ssim.load_species(sid, DeviceParticles(*[a[perm] for a in p.arrays()], p.ids[perm],
+                                               species_id=p.species_id))
+        del perm
+    ssim.set_fields(fields.E, fields.B)
+    ssim.run_cycle()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ks = 3
+    e0.record()
+    for _ in range(ks):
+        ssim.run_cycle()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del ssim
+    torch.cuda.empty_cache()
+    return {"value": n_total * ks / (float(t) * 1e-3), "unit": UNIT, "steps": ks,
+            "note": "flat layout, every species randomly permuted, no sort"}
 
 
 def e2e_cycle_leg(args, sim, fields, dist, dev, n_total):

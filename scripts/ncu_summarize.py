@@ -14,7 +14,12 @@ WANT = {"gpu__time_duration.sum": "gpu_time_ms_under_ncu", "smsp__inst_executed.
 SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out_path = os.path.join(P, f"ncu_summary_{R}.json")
 summary = json.load(open(out_path)) if os.path.exists(out_path) else {}
-for key, rep in (("mover", f"mover_f32_{R}"), ("deposit", f"deposit_f32_{R}"), ("span_kernel_parity", f"span_parity_{R}")):
+# key=report pairs after the round tag (reports gpurun_out/<report>.ncu-rep);
+# default: the round-1 captures of scripts/profile_bench.sh
+PAIRS = [a.split("=", 1) for a in sys.argv[2:]] or [
+    ("mover", f"mover_f32_{R}"), ("deposit", f"deposit_f32_{R}"),
+    ("span_kernel_parity", f"span_parity_{R}")]
+for key, rep in PAIRS:
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -22,7 +27,7 @@ for key, rep in (("mover", f"mover_f32_{R}"), ("deposit", f"deposit_f32_{R}"), (
     rows = list(csv.reader(raw.splitlines()))
     h, u, v = rows[0], rows[1], rows[2]
     d = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else key,
-         "capture": f"scripts/profile_bench.sh {R}"}
+         "capture": f"gpurun_out/{rep}.ncu-rep (round {R})"}
     for m, name in WANT.items():
         if m in h:
             i = h.index(m)
