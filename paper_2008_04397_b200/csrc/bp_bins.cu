@@ -227,6 +227,20 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
   return ST_OK;
 }
 
+// Speed bound below which no position of a push from cell q can leave the
+// box (interior() of bp_f32_common.cuh, per bin instead of per particle): a
+// particle of cell (i, j, k) lies at least min(i, n - 1 - i) cells from the
+// faces of each axis, and every midpoint and the committed position lie
+// within dt (|v|_1 + |qdt2m| max|E|) of the start; 1e-4 of the distance
+// (hmin = 0.9999 x the smallest spacing) and bc_eps cover the rounding.  A
+// bin touching a face gets a negative bound: every push there checks.
+__device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, float hmin,
+                                                 float epsmax) {
+  const int cells = min(min(min(q.i, a.nx - 1 - q.i), min(q.j, a.ny - 1 - q.j)),
+                        min(q.k, a.nz - 1 - q.k));
+  return __fdividef(fmaf((float)cells, hmin, -epsmax), a.dt) - qe;
+}
+
 // ---------------------------------------------------------------------------
 // Mover: one warp per bin.  A warp claims kMoveClaim consecutive bins; their
 // cell records (contiguous: records are in cell order) are staged in shared
@@ -250,6 +264,9 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
   unsigned long long* const bars = bars_s[wid];
   const unsigned lt = lanemask_lt();
   const float qe = fabsf(a.qdt2m) * __ldg(a.emax) * 1.00001f;
+  const float hmin = 0.9999f * fminf(fminf(a.L[0] / (float)a.nx, a.L[1] / (float)a.ny),
+                                     a.L[2] / (float)a.nz);
+  const float epsmax = fmaxf(fmaxf(a.bc_eps[0], a.bc_eps[1]), a.bc_eps[2]);
   const float4* const rec_g = static_cast<const float4*>(a.rec);
   if (lane == 0) {
     mbar_init(&bars[0], 1);
@@ -313,7 +330,7 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
         const float4* rs = recs_s[wid][bf] + (c - c0) * 12;
 #pragma unroll
         for (int q = 0; q < 12; ++q) R[q] = rs[q];
-        const Box bx = cell_box(a, q3);
+        const float vmax = bin_speed_bound(a, q3, qe, hmin, epsmax);
         int held = c;
         int nh = 0;
 #pragma unroll 1
@@ -335,18 +352,17 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
             }
           }
           const bool all_in =
-              __all_sync(0xffffffffu, sk::interior(a, qe, xp, yp, zp, un, vn, wn));
+              __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
           const int st = push_bin<RX, RY, RZ>(a, R, held, c, rs, xp, yp, zp, un, vn, wn, all_in);
           int dest = c;
           if (st == ST_OK) {
+            // the new cell (cell_of's formula, bp_f32_common.cuh)
             const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
             const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
             const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
-            if (!in_box(bx, gx, gy, gz)) {
-              const int i = min((int)gx, a.nx - 1), j = min((int)gy, a.ny - 1),
-                        k = min((int)gz, a.nz - 1);
-              dest = i + a.nx * j + a.cny * k;
-            }
+            const int i = min((int)gx, a.nx - 1), j = min((int)gy, a.ny - 1),
+                      k = min((int)gz, a.nz - 1);
+            dest = i + a.nx * j + a.cny * k;
           } else if (valid) {
             atomicMax(a.status, st);  // not stored (kernels.py:618-621); the cycle raises
           }

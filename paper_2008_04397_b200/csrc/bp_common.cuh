@@ -425,6 +425,7 @@ __device__ __forceinline__ void deposit_tile(Slot& A, Slot& Bs, i64* __restrict_
     }
   }
   if (strays) {
+    __syncwarp();  // every lane is done reading the staged rows
     if ((strays >> lane) & 1u) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) st_bs[c * kRow + lane] = 0.0;

@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(256, MINB) deposit_kernel(const __grid_constan
         __syncwarp();
         // the cell's patch values are read first (no alias with the staged
         // rows) so their latency hides behind the fold
-        const T o0 = pv0[kg], o1 = pv1[kg], o2 = pv2[kg];
+        // (moment 8 + (g & 1) is owned by the lanes of groups 0 and 1)
+        const T o0 = pv0[kg], o1 = pv1[kg], o2 = third ? pv2[kg] : T(0);
         // members software-pipelined: the next member's loads are issued
         // before this member's products
         unsigned m = MG;
