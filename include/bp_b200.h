@@ -205,10 +205,12 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  * reference's phase 3 + phase 6 pair, run_cycle's per-batch fused_span calls
  * (pipeline.py:178-268, kernels.py:458-735) and the periodic stable cell sort
  * (pipeline.py:300-304, particles.py:157-167), for one species at a time:
- * cell c owns slots [start[c], start[c+1]) of the SoA arrays, the first
- * count[c] live; every bp_bins_cycle leaves each particle in its cell's bin,
- * so the order is cell-sorted every cycle.  Particles, start, count, the
- * leaver / overflow lists, stat, records, acc, invvol: DEVICE pointers.
+ * the particles are 32-byte records (float x y z u | v w q 0, 16-byte
+ * aligned; rec) with an int64 id array; cell c owns slots [start[c],
+ * start[c+1]), the first count[c] live; every bp_bins_cycle leaves each
+ * particle in its cell's bin, so the order is cell-sorted every cycle.
+ * Records, ids, start, count, the leaver / overflow lists, stat, field
+ * records, acc, invvol: DEVICE pointers.
  *
  * bp_bins_plan   histogram of the flat arrays' cells (the fast kernels' f32
  *                cell formula) into count[ncell]; start[ncell + 1] = exclusive
@@ -216,7 +218,8 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  *                *total = start[ncell] (host int64; the call synchronises).
  *                Returns 3 (BP_ERR_DOMAIN) for positions below the origin.
  * bp_bins_fill   stable scatter of the flat arrays (x y z u v w q, ids) into
- *                dst[7] / dst_ids of start[ncell] slots (synchronises).
+ *                the records dst_rec / dst_ids of start[ncell] slots
+ *                (synchronises).
  * bp_bins_cycle  mover + leaver migration + 10-moment deposit of the bins
  *                into acc (+=); leavers / overflow / late are lists of
  *                bp_bins_leaver_bytes() records (the leaver list is scratch
@@ -234,10 +237,11 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  *                in cell order): with dst == NULL, new_count = live +
  *                overflow arrivals per bin and new_start = the padded layout,
  *                *total = new_start[ncell] (synchronises); with dst, the
- *                bins and the overflow list are copied into dst / dst_ids
+ *                bins and the overflow list are copied into dst_rec / dst_ids
  *                (new_count becomes the new live counts; synchronises).
  * bp_bins_export the live particles in cell order, then the overflow list,
- *                to flat dst[7] / dst_ids (dst == NULL: count only);
+ *                to the flat (reference SoA) arrays dst[7] / dst_ids
+ *                (dst == NULL: count only; dst itself is a host table);
  *                offsets[ncell + 1] = exclusive scan of the clamped counts;
  *                *total = particles (synchronises).
  */
@@ -253,20 +257,20 @@ int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int
 int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
                  const void* vs, const void* ws, const void* qs, const int64_t* ids, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
-                 const int64_t* start, void* const* dst, int64_t* dst_ids, void* stream);
-int bp_bins_cycle(int fbytes, float* xs, float* ys, float* zs, float* us, float* vs, float* ws,
-                  float* qs, int64_t* ids, const int64_t* start, int32_t* count, int64_t ncell,
+                 const int64_t* start, void* dst_rec, int64_t* dst_ids, void* stream);
+int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+                  int64_t ncell,
                   void* leavers, int64_t leaver_cap, void* overflow, int64_t overflow_cap,
                   void* late, int64_t late_cap, uint64_t* stat, const void* records,
                   int64_t* acc, const void* invvol,
                   const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
                   double dth, double qdt2m, double beta, double one, int n_iters, double scale,
                   int* d_status, void* stream);
-int bp_bins_reslack(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_reslack(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                     int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                     double slack_frac, int slack_min, int32_t* new_count, int64_t* new_start,
-                    void* const* dst, int64_t* dst_ids, int64_t* total, void* stream);
-int bp_bins_export(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+                    void* dst_rec, int64_t* dst_ids, int64_t* total, void* stream);
+int bp_bins_export(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream);

@@ -73,8 +73,8 @@ _SIGS = {
     "bp_bins_leaver_bytes": (_INT, []),
     "bp_bins_plan": (_INT, [_INT, _P, _P, _P, _I64, _P, _P, _P, _D, _INT, _P, _P, _P, _P]),
     "bp_bins_fill": (_INT, [_INT] + [_P] * 8 + [_I64, _P, _P, _P, _P, _P, _P, _P]),
-    "bp_bins_cycle": (_INT, [_INT] + [_P] * 10 + [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,
-                                                   _P, _P]
+    "bp_bins_cycle": (_INT, [_INT] + [_P] * 4 + [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,
+                                                  _P, _P]
                       + [_P, _P, _P] + [_D] * 5 + [_INT, _D, _P, _P]),
     "bp_init_maxwellian": (_INT, [_INT, ctypes.c_uint64, ctypes.c_uint64] + [_P] * 3
                            + [_INT] + [_P] * 3 + [_I64, _I64] + [_P] * 10 + [_I64, _P, _P]),

@@ -3,8 +3,9 @@
 
 The reference restores cell order with a stable sort every ``sort_period``
 cycles (particles.py:157-167, pipeline.py:300-304).  Here cell ``c`` owns
-slots ``[start[c], start[c + 1])`` of the SoA arrays (the reference's
-ParticleBuffer columns x y z u v w q_p and the int64 ids), the first
+slots ``[start[c], start[c + 1])`` of 32-byte particle records (the
+reference's ParticleBuffer columns x y z u v w q_p, then 0) and of the int64
+ids, the first
 ``count[c]`` of them live, and every cycle (``bp_bins_cycle``: mover, leaver
 migration, deposit) leaves each particle in its cell's bin — cell-sorted at
 every cycle.  ``flat()`` exports the live particles (cell order) as a
@@ -82,23 +83,23 @@ class BinnedSpecies:
             raise DomainError("positions below the box origin")
         cap = int(total.value)
         self.cap = cap
-        self.arrs, self.ids = self._alloc_set(cap)
+        self.rec, self.ids = self._alloc_set(cap)
         # the re-slack's destination, allocated now: a re-slack inside a run
         # then only copies (no multi-GB allocation in the middle of a cycle)
         self._spare = self._alloc_set(cap)
-        dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in self.arrs])
         rc = L.bp_bins_fill(self.fbytes, *[_ptr(a) for a in parts.arrays()], _ptr(parts.ids),
-                            parts.n, gf, gg, gi, _ptr(self.start), dst, _ptr(self.ids),
+                            parts.n, gf, gg, gi, _ptr(self.start), _ptr(self.rec), _ptr(self.ids),
                             ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_fill")
         self.n = parts.n
 
     def _alloc_set(self, cap):
-        """One buffer set (x..q, ids) for `cap` slots plus headroom (3% + 64k
-        slots), so that the slightly larger layouts of later re-slacks fit."""
+        """One buffer set (32-byte records x y z u | v w q 0, int64 ids) for
+        `cap` slots plus headroom (3% + 64k slots), so that the slightly
+        larger layouts of later re-slacks fit."""
         torch = self.torch
         n = int(cap * 1.03) + (1 << 16)
-        return ([torch.empty(n, dtype=torch.float32, device=self.device) for _ in ARRAYS],
+        return (torch.empty(8 * n, dtype=torch.float32, device=self.device),
                 torch.empty(n, dtype=torch.int64, device=self.device))
 
     def flat(self, stream=None):
@@ -107,10 +108,9 @@ class BinnedSpecies:
         torch = self.torch
         L = _lib.load()
         s = self._stream(stream)
-        src = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in self.arrs])
         off = torch.empty(self.ncell + 1, dtype=torch.int64, device=self.device)
         total = ctypes.c_int64(0)
-        args = (src, _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
+        args = (_ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
                 _ptr(self.overflow), self.overflow_cap, _ptr(self.stat))
         rc = L.bp_bins_export(*args, _ptr(off), None, None, ctypes.byref(total),
                               ctypes.c_void_p(s.cuda_stream))
@@ -140,11 +140,10 @@ class BinnedSpecies:
         torch = self.torch
         L = _lib.load()
         s = self._stream(stream)
-        src = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in self.arrs])
         ncount = torch.empty(self.ncell, dtype=torch.int32, device=self.device)
         nstart = torch.empty(self.ncell + 1, dtype=torch.int64, device=self.device)
         total = ctypes.c_int64(0)
-        args = (src, _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
+        args = (_ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
                 _ptr(self.overflow), self.overflow_cap, _ptr(self.stat), self.slack[0],
                 self.slack[1], _ptr(ncount), _ptr(nstart))
         rc = L.bp_bins_reslack(*args, None, None, ctypes.byref(total),
@@ -154,12 +153,11 @@ class BinnedSpecies:
         spare = self._spare
         if spare[1].numel() < cap:
             spare = self._alloc_set(cap)
-        dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in spare[0]])
-        rc = L.bp_bins_reslack(*args, dst, _ptr(spare[1]), ctypes.byref(total),
+        rc = L.bp_bins_reslack(*args, _ptr(spare[0]), _ptr(spare[1]), ctypes.byref(total),
                                ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_reslack")
-        self._spare = (self.arrs, self.ids)
-        self.arrs, self.ids = spare
+        self._spare = (self.rec, self.ids)
+        self.rec, self.ids = spare
         self.start, self.count, self.cap = nstart, ncount, cap
         self.stat.zero_()
         self.rebuilds += 1
@@ -171,9 +169,8 @@ class BinnedSpecies:
     def cycle(self, lists, records, acc, invvol, sc, n_iters, scale, d_status, stream):
         """Mover + migration + deposit of this species (asynchronous)."""
         L = _lib.load()
-        a = self.arrs
         gf, gg, gi = (ctypes.c_void_p(x.ctypes.data) for x in (self.geo_f, self.geo_g, self.geo_i))
-        rc = L.bp_bins_cycle(self.fbytes, *[_ptr(t) for t in a], _ptr(self.ids), _ptr(self.start),
+        rc = L.bp_bins_cycle(self.fbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start),
                              _ptr(self.count), self.ncell, _ptr(lists.leavers), lists.leaver_cap,
                              _ptr(self.overflow), self.overflow_cap, _ptr(self.late),
                              self.late_cap, _ptr(self.stat),

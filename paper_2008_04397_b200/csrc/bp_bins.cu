@@ -74,7 +74,7 @@ enum {
 };
 
 struct Bins {
-  float *x, *y, *z, *u, *v, *w, *q;
+  float4* rec;  // 2 per slot: x y z u | v w q 0 (32-byte particle records)
   long long* id;
   const long long* start;  // [ncell + 1]
   int* count;              // [ncell]
@@ -87,6 +87,30 @@ struct Bins {
   long long late_cap;
   unsigned long long* stat;  // [ST_N]
 };
+
+// one 32-byte particle record per thread: a single 256-bit access (sm_100
+// ld/st .v8), so the lanes of a warp cover whole sectors with one instruction
+__device__ __forceinline__ void ld_rec_stream(const float4* p, float4& a, float4& b) {
+  asm volatile("ld.global.L1::evict_first.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_rec_ro(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void st_rec_stream(float4* p, const float4& a, const float4& b) {
+  asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_rec(float4* p, const float4& a, const float4& b) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x),
+               "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
 
 constexpr int kHoleCap = 64;     // leavers per bin per cycle tracked for the refill
 constexpr int kMoveClaim = 8;    // bins per mover work claim
@@ -297,12 +321,11 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
   int bf = 0;
   int c0 = claim(0);
   // prefetched particle (one per lane) and the slot it came from
-  float n1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float4 n1a = make_float4(0.f, 0.f, 0.f, 0.f), n1b = n1a;
   auto fetch = [&](long long q, bool ok) {
     if (ok) {
-      // streaming loads (read once per cycle)
-      n1[0] = __ldcs(b.x + q); n1[1] = __ldcs(b.y + q); n1[2] = __ldcs(b.z + q);
-      n1[3] = __ldcs(b.u + q); n1[4] = __ldcs(b.v + q); n1[5] = __ldcs(b.w + q);
+      // streaming loads (read once per cycle): the 32-byte record
+      ld_rec_stream(b.rec + 2 * q, n1a, n1b);
     }
   };
   float4 R[12];
@@ -338,7 +361,8 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
           const int r = t0 + (int)lane;
           const bool valid = r < n;
           const long long p = s0 + r;
-          float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5];
+          float xp = n1a.x, yp = n1a.y, zp = n1a.z, un = n1a.w, vn = n1b.x, wn = n1b.y;
+          const float qp = n1b.z;
           if (t0 + 32 < n) fetch(p + 32, r + 32 < n);
           else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1);
           if (n - t0 < 32) {
@@ -388,11 +412,11 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
           // with the rank), so their hole indices stay contiguous
           listed = leave && slot < b.lv_cap && nh + rank < kHoleCap;
           if (listed) {
-            // q and id are added at the end of the bin (one load latency
-            // per bin instead of per tile)
+            // the id is added at the end of the bin (one load latency per
+            // bin instead of per tile)
             float4* rec = reinterpret_cast<float4*>(b.lv + slot);
             rec[0] = make_float4(xp, yp, zp, un);
-            rec[1] = make_float4(vn, wn, 0.f, __int_as_float(dest));
+            rec[1] = make_float4(vn, wn, qp, __int_as_float(dest));
             holes[nh + rank] = r;
             lvslot[nh + rank] = slot;
           } else if (leave) {
@@ -413,13 +437,12 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
         // written; write-back stores, so the refill and the migration find
         // the bin's lines in L2
         if (valid && st == ST_OK) {
-          __stcs(b.x + p, xp); __stcs(b.y + p, yp); __stcs(b.z + p, zp);
-          __stcs(b.u + p, un); __stcs(b.v + p, vn); __stcs(b.w + p, wn);
+          st_rec_stream(b.rec + 2 * p, make_float4(xp, yp, zp, un), make_float4(vn, wn, qp, 0.f));
         }
       }
         __syncwarp();
         if (nh > 0) {
-          // leavers' q and id into their records; refill: the holes below the
+          // leavers' ids into their records; refill: the holes below the
           // new count take the trailing stayers (holes are ascending; the
           // k-th trailing stayer is the k-th slot >= n_stay that is not a
           // hole).  All loads are issued before any store: the refill writes
@@ -433,15 +456,10 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
           for (int k0 = 0; k0 < nh; k0 += 32) {
             const int k = k0 + (int)lane;
             // this lane's leaver (k < nh) and refill pair (k < nlow)
-            float lq = 0.f;
             long long lid = 0;
-            if (k < nh) {
-              const long long hp = s0 + holes[k];
-              lq = b.q[hp];
-              lid = b.id[hp];
-            }
+            if (k < nh) lid = b.id[s0 + holes[k]];
             long long src = 0, dst = 0;
-            float rx = 0.f, ry = 0.f, rz = 0.f, ru = 0.f, rv = 0.f, rw = 0.f, rq = 0.f;
+            float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
             long long rid = 0;
             if (k < nlow) {
               int t = n_stay + k;
@@ -451,20 +469,16 @@ __global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a
               }
               src = s0 + t;
               dst = s0 + holes[k];
-              rx = b.x[src]; ry = b.y[src]; rz = b.z[src];
-              ru = b.u[src]; rv = b.v[src]; rw = b.w[src];
-              rq = b.q[src]; rid = b.id[src];
+              ra = b.rec[2 * src];
+              rb = b.rec[2 * src + 1];
+              rid = b.id[src];
             }
-            if (k < nh) {
-              float* rec = reinterpret_cast<float*>(b.lv + lvslot[k]);
-              rec[6] = lq;
-              *reinterpret_cast<long long*>(rec + 8) = lid;
-            }
+            if (k < nh) b.lv[lvslot[k]].id = lid;
             __syncwarp();
             if (k < nlow) {
-              b.x[dst] = rx; b.y[dst] = ry; b.z[dst] = rz;
-              b.u[dst] = ru; b.v[dst] = rv; b.w[dst] = rw;
-              b.q[dst] = rq; b.id[dst] = rid;
+              b.rec[2 * dst] = ra;
+              b.rec[2 * dst + 1] = rb;
+              b.id[dst] = rid;
             }
           }
         if (lane == 0) b.count[c] = n_stay;
@@ -497,9 +511,9 @@ __global__ void __launch_bounds__(256) migrate_bins(const __grid_constant__ Bins
     const long long s = b.start[dest];
     if (pos < b.start[dest + 1] - s) {
       const long long d = s + pos;
-      b.x[d] = L.a.x; b.y[d] = L.a.y; b.z[d] = L.a.z;
-      b.u[d] = L.a.w; b.v[d] = L.b.x; b.w[d] = L.b.y;
-      b.q[d] = L.b.z; b.id[d] = L.id;
+      // one full 32-byte sector (no partial-sector read-modify-write)
+      st_rec(b.rec + 2 * d, L.a, make_float4(L.b.x, L.b.y, L.b.z, 0.f));
+      b.id[d] = L.id;
     } else {
       const unsigned long long o = atomicAdd(&b.stat[ST_OVERFLOW], 1ULL);
       if ((long long)o < b.ov_cap) b.ov[o] = L;
@@ -567,9 +581,10 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
   auto fetch = [&](long long q, bool ok) {
     if (ok) {
       // read-only path (measured faster than streaming loads here)
-      n1[0] = __ldg(b.x + q); n1[1] = __ldg(b.y + q); n1[2] = __ldg(b.z + q);
-      n1[3] = __ldg(b.u + q); n1[4] = __ldg(b.v + q); n1[5] = __ldg(b.w + q);
-      n1[6] = __ldg(b.q + q);
+      float4 ra, rb;
+      ld_rec_ro(b.rec + 2 * q, ra, rb);
+      n1[0] = ra.x; n1[1] = ra.y; n1[2] = ra.z; n1[3] = ra.w;
+      n1[4] = rb.x; n1[5] = rb.y; n1[6] = rb.z;
     }
   };
   for (;;) {
@@ -737,14 +752,14 @@ __global__ void bin_scatter(const unsigned* __restrict__ skeys,
                             const unsigned* __restrict__ sidx, long long n,
                             const long long* __restrict__ start,
                             const long long* __restrict__ first, const float* const* src,
-                            const long long* __restrict__ sid, float* const* dst,
+                            const long long* __restrict__ sid, float4* __restrict__ drec,
                             long long* __restrict__ did) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
     const unsigned k = skeys[r], j = sidx[r];
     const long long d = start[k] + (r - first[k]);
-#pragma unroll
-    for (int a = 0; a < 7; ++a) dst[a][d] = src[a][j];
+    drec[2 * d] = make_float4(src[0][j], src[1][j], src[2][j], src[3][j]);
+    drec[2 * d + 1] = make_float4(src[4][j], src[5][j], src[6][j], 0.f);
     did[d] = sid[j];
   }
 }
@@ -755,14 +770,14 @@ __global__ void bin_export(const __grid_constant__ Bins b, const long long* __re
   const int lane = threadIdx.x & 31;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const float* src[7] = {b.x, b.y, b.z, b.u, b.v, b.w, b.q};
   for (long long c = gw; c < b.ncell; c += nw) {
     const long long s0 = b.start[c];
     const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
     const long long o = off[c];
     for (int r = lane; r < n; r += 32) {
-#pragma unroll
-      for (int a = 0; a < 7; ++a) dst[a][o + r] = src[a][s0 + r];
+      const float4 x = b.rec[2 * (s0 + r)], y = b.rec[2 * (s0 + r) + 1];
+      dst[0][o + r] = x.x; dst[1][o + r] = x.y; dst[2][o + r] = x.z; dst[3][o + r] = x.w;
+      dst[4][o + r] = y.x; dst[5][o + r] = y.y; dst[6][o + r] = y.z;
       did[o + r] = b.id[s0 + r];
     }
   }
@@ -810,26 +825,26 @@ __global__ void reslack_hist(const __grid_constant__ Bins b, int* __restrict__ n
 }
 // warp per bin: live particles to the new layout; ncount = live count
 __global__ void reslack_copy(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
-                             int* __restrict__ ncount, float* const* dst,
+                             int* __restrict__ ncount, float4* __restrict__ drec,
                              long long* __restrict__ did) {
   const int lane = threadIdx.x & 31;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const float* src[7] = {b.x, b.y, b.z, b.u, b.v, b.w, b.q};
   for (long long c = gw; c < b.ncell; c += nw) {
     const long long s0 = b.start[c];
     const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
     const long long d0 = nstart[c];
     for (int r = lane; r < n; r += 32) {
 #pragma unroll
-      for (int a = 0; a < 7; ++a) __stcs(dst[a] + d0 + r, __ldcs(src[a] + s0 + r));
+      __stcs(drec + 2 * (d0 + r), __ldcs(b.rec + 2 * (s0 + r)));
+      __stcs(drec + 2 * (d0 + r) + 1, __ldcs(b.rec + 2 * (s0 + r) + 1));
       __stcs(did + d0 + r, __ldcs(b.id + s0 + r));
     }
     if (lane == 0) ncount[c] = n;
   }
 }
 __global__ void reslack_place(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
-                              int* __restrict__ ncount, float* const* dst,
+                              int* __restrict__ ncount, float4* __restrict__ drec,
                               long long* __restrict__ did) {
   const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -838,8 +853,8 @@ __global__ void reslack_place(const __grid_constant__ Bins b, const long long* _
     const int dest = __float_as_int(L.b.w);
     if (dest < 0 || dest >= b.ncell) continue;
     const long long d = nstart[dest] + atomicAdd(ncount + dest, 1);
-    dst[0][d] = L.a.x; dst[1][d] = L.a.y; dst[2][d] = L.a.z; dst[3][d] = L.a.w;
-    dst[4][d] = L.b.x; dst[5][d] = L.b.y; dst[6][d] = L.b.z;
+    drec[2 * d] = L.a;
+    drec[2 * d + 1] = make_float4(L.b.x, L.b.y, L.b.z, 0.f);
     did[d] = L.id;
   }
 }
@@ -911,9 +926,7 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   a.emax = reinterpret_cast<const float*>(
       (const char*)c.records + (split_records_bytes(4, c.geo_i) - 32));
   bins::Bins b;
-  b.x = (float*)c.x; b.y = (float*)c.y; b.z = (float*)c.z;
-  b.u = (float*)c.u; b.v = (float*)c.v; b.w = (float*)c.w;
-  b.q = (float*)const_cast<void*>(c.q);
+  b.rec = (float4*)ba.rec;
   b.id = (long long*)ba.ids;
   b.start = (const long long*)ba.start;
   b.count = ba.count;
@@ -992,7 +1005,7 @@ int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin,
 }
 
 // Build step 2: stable scatter of the flat span into the planned bins.
-int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* const* dst,
+int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
               int64_t* dst_ids, cudaStream_t s) {
   bins::P a;
   fill_params<float>(c, a);
@@ -1042,13 +1055,13 @@ int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void*
   const void* hp[16] = {(const float*)c.x + c.start, (const float*)c.y + c.start,
                         (const float*)c.z + c.start, (const float*)c.u + c.start,
                         (const float*)c.v + c.start, (const float*)c.w + c.start,
-                        (const float*)c.q + c.start, dst[0], dst[1], dst[2], dst[3], dst[4],
-                        dst[5], dst[6], nullptr, nullptr};
+                        (const float*)c.q + c.start, nullptr, nullptr, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaMemcpyAsync(ptrs, hp, sizeof(hp), cudaMemcpyHostToDevice, s);
   bins::bin_scatter<<<nsm() * 8, 256, 0, s>>>(k_out, i_out, n, (const long long*)start, first,
                                               (const float* const*)ptrs,
                                               (const long long*)src_ids + c.start,
-                                              (float* const*)(ptrs + 7), (long long*)dst_ids);
+                                              (float4*)dst_rec, (long long*)dst_ids);
   note_launch();
   cudaFreeAsync(ws, s);
   int rc = bcheck("bins_fill");
@@ -1060,12 +1073,10 @@ int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void*
 // Live-particle offsets of the bins (exclusive scan of the clamped counts)
 // and the flat copy; the overflow list follows at the end.  Returns the
 // particle total through *total (synchronises).
-int bins_export(const BinsArgs& ba, void* const* src, int64_t* offsets, void* const* dst,
+int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void* const* dst,
                 int64_t* dst_ids, int64_t* total, cudaStream_t s) {
   bins::Bins b{};
-  b.x = (float*)src[0]; b.y = (float*)src[1]; b.z = (float*)src[2];
-  b.u = (float*)src[3]; b.v = (float*)src[4]; b.w = (float*)src[5];
-  b.q = (float*)src[6];
+  b.rec = (float4*)const_cast<void*>(src_rec);
   b.id = (long long*)ba.ids;
   b.start = (const long long*)ba.start;
   b.count = ba.count;
@@ -1125,11 +1136,9 @@ int bins_export(const BinsArgs& ba, void* const* src, int64_t* offsets, void* co
 namespace bp {
 
 namespace {
-bins::Bins bins_of(const BinsArgs& ba, void* const* src) {
+bins::Bins bins_of(const BinsArgs& ba, const void* src_rec) {
   bins::Bins b{};
-  b.x = (float*)src[0]; b.y = (float*)src[1]; b.z = (float*)src[2];
-  b.u = (float*)src[3]; b.v = (float*)src[4]; b.w = (float*)src[5];
-  b.q = (float*)src[6];
+  b.rec = (float4*)const_cast<void*>(src_rec);
   b.id = (long long*)ba.ids;
   b.start = (const long long*)ba.start;
   b.count = ba.count;
@@ -1143,9 +1152,9 @@ bins::Bins bins_of(const BinsArgs& ba, void* const* src) {
 
 // Re-slack plan: ncount = live + overflow arrivals per bin, nstart = exclusive
 // scan of the padded capacities; *total = nstart[ncell] (synchronises).
-int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t* nstart,
+int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
                       double frac, int smin, int64_t* total, cudaStream_t s) {
-  const bins::Bins b = bins_of(ba, src);
+  const bins::Bins b = bins_of(ba, src_rec);
   const int ncell = b.ncell;
   bins::reslack_counts<<<nsm() * 4, 256, 0, s>>>(b, ncount);
   note_launch();
@@ -1174,22 +1183,15 @@ int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t
 
 // Re-slack copy into dst (nstart from the plan); ncount ends as the new
 // live counts (synchronises).
-int bins_reslack_copy(const BinsArgs& ba, void* const* src, const int64_t* nstart, int* ncount,
-                      void* const* dst, int64_t* dst_ids, cudaStream_t s) {
-  const bins::Bins b = bins_of(ba, src);
-  void** ptrs = nullptr;
-  if (cudaMallocAsync(&ptrs, 8 * sizeof(void*), s) != cudaSuccess) {
-    set_error("bins_reslack_copy: scratch allocation failed");
-    return -2;
-  }
-  cudaMemcpyAsync(ptrs, dst, 7 * sizeof(void*), cudaMemcpyHostToDevice, s);
+int bins_reslack_copy(const BinsArgs& ba, const void* src_rec, const int64_t* nstart,
+                      int* ncount, void* dst_rec, int64_t* dst_ids, cudaStream_t s) {
+  const bins::Bins b = bins_of(ba, src_rec);
   bins::reslack_copy<<<nsm() * 8, 256, 0, s>>>(b, (const long long*)nstart, ncount,
-                                               (float* const*)ptrs, (long long*)dst_ids);
+                                               (float4*)dst_rec, (long long*)dst_ids);
   note_launch();
   bins::reslack_place<<<nsm() * 2, 256, 0, s>>>(b, (const long long*)nstart, ncount,
-                                                (float* const*)ptrs, (long long*)dst_ids);
+                                                (float4*)dst_rec, (long long*)dst_ids);
   note_launch();
-  cudaFreeAsync(ptrs, s);
   int rc = bcheck("bins_reslack_copy");
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_reslack_copy sync");
   return rc;

@@ -702,24 +702,20 @@ int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int
 int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
                  const void* vs, const void* ws, const void* qs, const int64_t* ids, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
-                 const int64_t* start, void* const* dst, int64_t* dst_ids, void* stream) {
+                 const int64_t* start, void* dst_rec, int64_t* dst_ids, void* stream) {
   Call c{};
   int rc = bins_call(c, fbytes, xs, ys, zs, us, vs, ws, qs, 0, n, geo_f, geo_g, geo_i);
   if (rc) return rc;
-  if (!ids || !start || !dst || !dst_ids || !qs) {
-    set_error("bins_fill: bad arguments");
+  if (!ids || !start || !dst_rec || ((uintptr_t)dst_rec % 16) != 0 || !dst_ids || !us || !vs ||
+      !ws || !qs) {
+    set_error("bins_fill: bad arguments (16-byte aligned records)");
     return BP_EINVAL;
   }
-  for (int k = 0; k < 7; ++k)
-    if (!dst[k]) {
-      set_error("bins_fill: destination array %d missing", k);
-      return BP_EINVAL;
-    }
-  return bins_fill(c, ids, start, dst, dst_ids, (cudaStream_t)stream);
+  return bins_fill(c, ids, start, dst_rec, dst_ids, (cudaStream_t)stream);
 }
 
-int bp_bins_cycle(int fbytes, float* xs, float* ys, float* zs, float* us, float* vs, float* ws,
-                  float* qs, int64_t* ids, const int64_t* start, int32_t* count, int64_t ncell,
+int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+                  int64_t ncell,
                   void* leavers, int64_t leaver_cap, void* overflow, int64_t overflow_cap,
                   void* late, int64_t late_cap, uint64_t* stat, const void* records,
                   int64_t* acc, const void* invvol,
@@ -727,9 +723,10 @@ int bp_bins_cycle(int fbytes, float* xs, float* ys, float* zs, float* us, float*
                   double dth, double qdt2m, double beta, double one, int n_iters, double scale,
                   int* d_status, void* stream) {
   Call c{};
-  int rc = bins_call(c, fbytes, xs, ys, zs, us, vs, ws, qs, 0, 0, geo_f, geo_g, geo_i);
+  int rc = bins_call(c, fbytes, rec, rec, rec, rec, rec, rec, rec, 0, 0, geo_f, geo_g, geo_i);
   if (rc) return rc;
-  if (!records || ((uintptr_t)records % 32) != 0 || !acc || !invvol || !ids || !start ||
+  if (!rec || ((uintptr_t)rec % 16) != 0 || !records || ((uintptr_t)records % 32) != 0 ||
+      !acc || !invvol || !ids || !start ||
       !count || !stat || !leavers || !overflow || !late || leaver_cap < 0 ||
       overflow_cap < 0 || late_cap < 0 ||
       n_iters < 0 || !d_status) {
@@ -745,45 +742,47 @@ int bp_bins_cycle(int fbytes, float* xs, float* ys, float* zs, float* us, float*
   c.n_iters = n_iters; c.mixed = fbytes == 8; c.apply_bc = 1;
   c.records = records;
   c.status = d_status;
-  BinsArgs ba{ids,      start,        count, ncell, leavers, leaver_cap,
-              overflow, overflow_cap, stat,  late,  late_cap};
+  BinsArgs ba{rec,     ids,      start,        count, ncell, leavers,
+              leaver_cap, overflow, overflow_cap, stat,  late,  late_cap};
   return bins_cycle(c, ba, (cudaStream_t)stream);
 }
 
-int bp_bins_export(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_export(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream) {
-  if (!src || !ids || !start || !count || !offsets || !total || ncell <= 0) {
+  if (!rec || ((uintptr_t)rec % 16) != 0 || !ids || !start || !count || !offsets || !total ||
+      ncell <= 0) {
     set_error("bins_export: bad arguments");
     return BP_EINVAL;
   }
   ensure_pool();
-  BinsArgs ba{ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
+  BinsArgs ba{nullptr, ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
               overflow ? overflow_cap : 0, stat, nullptr, 0};
-  return bins_export(ba, (void* const*)src, offsets, dst, dst_ids, total, (cudaStream_t)stream);
+  return bins_export(ba, rec, offsets, dst, dst_ids, total, (cudaStream_t)stream);
 }
 
-int bp_bins_reslack(float* const* src, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_reslack(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                     int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                     double slack_frac, int slack_min, int32_t* new_count, int64_t* new_start,
-                    void* const* dst, int64_t* dst_ids, int64_t* total, void* stream) {
-  if (!src || !ids || !start || !count || !new_count || !new_start || !total || ncell <= 0 ||
-      slack_frac < 0 || slack_min < 0 || (overflow && !stat)) {
+                    void* dst_rec, int64_t* dst_ids, int64_t* total, void* stream) {
+  if (!rec || ((uintptr_t)rec % 16) != 0 || !ids || !start || !count || !new_count ||
+      !new_start || !total || ncell <= 0 || slack_frac < 0 || slack_min < 0 ||
+      (overflow && !stat)) {
     set_error("bins_reslack: bad arguments");
     return BP_EINVAL;
   }
   ensure_pool();
-  BinsArgs ba{ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
+  BinsArgs ba{nullptr, ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
               overflow ? overflow_cap : 0, stat, nullptr, 0};
-  if (!dst)
-    return bins_reslack_plan(ba, (void* const*)src, new_count, new_start, slack_frac, slack_min,
+  if (!dst_rec)
+    return bins_reslack_plan(ba, rec, new_count, new_start, slack_frac, slack_min,
                              total, (cudaStream_t)stream);
-  if (!dst_ids) {
-    set_error("bins_reslack: dst_ids required with dst");
+  if (!dst_ids || ((uintptr_t)dst_rec % 16) != 0) {
+    set_error("bins_reslack: dst_ids required with dst_rec (16-byte aligned)");
     return BP_EINVAL;
   }
-  return bins_reslack_copy(ba, (void* const*)src, new_start, new_count, dst, dst_ids,
+  return bins_reslack_copy(ba, rec, new_start, new_count, dst_rec, dst_ids,
                            (cudaStream_t)stream);
 }
 

@@ -46,6 +46,7 @@ int split_fused(const Call& c, const void* rec, cudaStream_t s);
 
 // Cell-binned f32 fast path (bp_bins.cu): the bin layout of one species
 struct BinsArgs {
+  void* rec;             // 32-byte particle records x y z u | v w q 0 per slot
   int64_t* ids;
   const int64_t* start;  // [ncell + 1] slot offsets
   int* count;            // [ncell] live particles per bin
@@ -62,14 +63,14 @@ constexpr int kBinsLeaverBytes = 48;
 int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s);
 int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
               cudaStream_t s);
-int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* const* dst,
+int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
               int64_t* dst_ids, cudaStream_t s);
-int bins_export(const BinsArgs& ba, void* const* src, int64_t* offsets, void* const* dst,
+int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void* const* dst,
                 int64_t* dst_ids, int64_t* total, cudaStream_t s);
-int bins_reslack_plan(const BinsArgs& ba, void* const* src, int* ncount, int64_t* nstart,
+int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
                       double frac, int smin, int64_t* total, cudaStream_t s);
-int bins_reslack_copy(const BinsArgs& ba, void* const* src, const int64_t* nstart, int* ncount,
-                      void* const* dst, int64_t* dst_ids, cudaStream_t s);
+int bins_reslack_copy(const BinsArgs& ba, const void* src_rec, const int64_t* nstart,
+                      int* ncount, void* dst_rec, int64_t* dst_ids, cudaStream_t s);
 
 // Bit-exact device loader (bp_init.cu): one species of the reference's
 // init_maxwellian on the cell range [c0, c0 + nc)
