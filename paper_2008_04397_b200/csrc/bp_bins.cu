@@ -274,13 +274,21 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 // the holes below the new count are refilled with the bin's trailing stayers
 // (about as many particle copies as leavers).  The next tile's particles
 // (across bins of the claim) are loaded while the current tile is pushed.
+#ifndef BP_MOVER_TPB
+#define BP_MOVER_TPB 128  // threads per block of mover_bins (measured: 128 x 5 > 256 x 2)
+#endif
+#ifndef BP_MOVER_MINB
+#define BP_MOVER_MINB 5   // resident blocks per SM it is compiled for (<= 102 registers)
+#endif
+constexpr int kMoverWarps = BP_MOVER_TPB / 32;
+
 template <bool RX, bool RY, bool RZ>
-__global__ void __launch_bounds__(256, 2) mover_bins(const __grid_constant__ P a,
+__global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const __grid_constant__ P a,
                                                      const __grid_constant__ Bins b) {
-  __shared__ __align__(128) float4 recs_s[8][2][kMoveClaim * 12];
-  __shared__ __align__(8) unsigned long long bars_s[8][2];
-  __shared__ int holes_s[8][kHoleCap];
-  __shared__ long long lvslot_s[8][kHoleCap];
+  __shared__ __align__(128) float4 recs_s[kMoverWarps][2][kMoveClaim * 12];
+  __shared__ __align__(8) unsigned long long bars_s[kMoverWarps][2];
+  __shared__ int holes_s[kMoverWarps][kHoleCap];
+  __shared__ long long lvslot_s[kMoverWarps][kHoleCap];
   const int wid = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
   int* const holes = holes_s[wid];
@@ -883,18 +891,18 @@ int nsm() {
 }
 
 template <typename K>
-int resident_grid(K k, size_t smem) {
+int resident_grid(K k, size_t smem, int threads = 256) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
   return nsm() * (per_sm < 1 ? 1 : per_sm);
 }
 
 template <bool RX, bool RY, bool RZ>
 int launch_mover_bins(const bins::P& a, const bins::Bins& b, cudaStream_t s) {
   auto k = bins::mover_bins<RX, RY, RZ>;
-  const int g = resident_grid(k, 0);
+  const int g = resident_grid(k, 0, BP_MOVER_TPB);
   const int th = timing_begin(TK_MOVER, s);
-  k<<<g, 256, 0, s>>>(a, b);
+  k<<<g, BP_MOVER_TPB, 0, s>>>(a, b);
   timing_end(th, s);
   note_launch();
   return bcheck("mover_bins launch");

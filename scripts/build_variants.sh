@@ -9,7 +9,7 @@ for spec in "$@"; do
   make -s -C "$ROOT/paper_2008_04397_b200/csrc" clean >/dev/null
   make -s -C "$ROOT/paper_2008_04397_b200/csrc" -j8 NVCC="nvcc $flags" >/dev/null 2>&1 || { echo "build $name failed"; exit 1; }
   cp "$ROOT/paper_2008_04397_b200/libbp_b200.so" "$ROOT/build_variants/lib_$name.so"
-  grep -A2 "cycle_bins" "$ROOT/paper_2008_04397_b200/csrc/bp_bins.ptxas.txt" | grep Used | head -1 | sed "s/^/$name: /"
+  grep -A2 "${KGREP:-mover_bins}" "$ROOT/paper_2008_04397_b200/csrc/bp_bins.ptxas.txt" | grep Used | head -1 | sed "s/^/$name: /"
 done
 make -s -C "$ROOT/paper_2008_04397_b200/csrc" clean >/dev/null
 make -s -C "$ROOT/paper_2008_04397_b200/csrc" -j8 >/dev/null 2>&1
