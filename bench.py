@@ -76,7 +76,16 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-shuffled", action="store_true")
+    ap.add_argument("--bin-slack", default=None,
+                    help="binned layout headroom 'frac,min' (DeviceSimulation.bin_slack)")
     return ap.parse_args()
+
+
+def slack_kw(args):
+    if not args.bin_slack:
+        return {}
+    f, m = args.bin_slack.split(",")
+    return {"bin_slack": (float(f), int(m))}
 
 
 def workload_config(args, world):
@@ -268,8 +277,10 @@ def main_ours(args):
     prec = PrecisionMode.from_label(args.precision)
     sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=args.arith,
                            sort_period=args.sort_period, device=dev, distributed=world > 1,
-                           layout=args.layout)
+                           layout=args.layout, **slack_kw(args))
     config["layout"] = "bins" if sim.binned else "flat"
+    if sim.binned:
+        config["bin_slack"] = list(sim.bin_slack)
     c0, nc = shard_span(geom.n_cells, rank, world)
     for sid, p in enumerate(init_gem_device(geom, species, dev, precision=prec, cells=(c0, nc))):
         sim.load_species(sid, p)

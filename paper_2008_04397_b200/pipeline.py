@@ -102,9 +102,10 @@ class DeviceSimulation:
     layout: str = "auto"
     # bin capacity = count + max(slack[1], slack[0] * count), rounded to 8
     # slots: a bin that fills up forces a re-slack of the species (a copy of
-    # all bins); 64 slots of minimum headroom keep that to every ~10 cycles at
-    # C3 (bins near the sheet fill by ~5 particles per cycle)
-    bin_slack: tuple = (0.5, 64)
+    # all bins, ~3 ms at C3); bins near the sheet gain ~5 particles per
+    # cycle, and doubling the capacity keeps re-slacks to a few per hundred
+    # cycles (memory: 2 buffer sets x 2 x 40 B per particle)
+    bin_slack: tuple = (1.0, 64)
 
     def __post_init__(self):
         import torch
