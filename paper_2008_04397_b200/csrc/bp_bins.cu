@@ -206,6 +206,7 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
     float fx, fy, fz;
     int i, j, k;
     const int cell = sk::cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    float ex, ey, hx, hy, ez, hz;
     const bool need = cell != held;
     if (__any_sync(0xffffffffu, need)) {
       if (need) {
@@ -218,7 +219,6 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
         }
       }
     }
-    float ex, ey, hx, hy, ez, hz;
     sk::tri_pair(R[0], R[1], R[2], R[3], fx, fy, fz, ex, ey);
     sk::tri_pair(R[4], R[5], R[6], R[7], fx, fy, fz, hx, hy);
     sk::tri_pair(R[8], R[9], R[10], R[11], fx, fy, fz, ez, hz);

@@ -276,10 +276,17 @@ __global__ void zig_emit(const __grid_constant__ Load L) {
   const long long nch = L.status[1];
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < nch;
        j += (long long)gridDim.x * blockDim.x) {
+    // normals k of this chunk: [kfirst[j], kfirst[j + 1]); skip the chunk
+    // unless it holds a normal of the shard (k mod n_p in [p0, p1))
+    const long long klo = L.kfirst[j], khi = j + 1 < nch ? L.kfirst[j + 1] : L.N;
+    bool hit = false;
+    for (int a = 0; a < 3 && !hit; ++a)
+      hit = klo < a * L.n_p + L.p1 && khi > a * L.n_p + L.p0;
+    if (!hit) continue;
     Stream S(L.k0, L.k1);
     const long long end = min((j + 1) * (long long)kChunk, L.M);
     long long p = j * (long long)kChunk + L.entry[j];
-    long long k = L.kfirst[j];
+    long long k = klo;
     while (p < end && k < L.N) {
       const Normal nm = normal_at(S, L.base + p);
       if (nm.len != (int)L.len[p]) atomicOr(L.status, 4);

@@ -10,12 +10,15 @@ import torch
 from paper_2008_04397_b200.config import PrecisionMode, SpeciesParams
 from paper_2008_04397_b200.gem import VTH_E, gem_geometry, init_uniform_device
 from paper_2008_04397_b200.pipeline import DeviceSimulation
+from bench import ClockMonitor
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="1e7,1e8,1e9")
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--modes", default="single,mixed,double")
 ap.add_argument("--ariths", default="fast,parity")
+ap.add_argument("--bin-slack", default="0.25,16",
+                help="binned-layout headroom (1e9 particles: two buffer sets must fit)")
 args = ap.parse_args()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -27,8 +30,9 @@ for n_target in (float(x) for x in args.sizes.split(",")):
         prec = PrecisionMode.from_label(mode)
         sp = (SpeciesParams(0, -1.0, 1.0 / 64.0, ppc, vth=(VTH_E,) * 3),)
         for arith in args.ariths.split(","):
+            fr, mn = args.bin_slack.split(",")
             sim = DeviceSimulation(geom, sp, dt=0.25, precision=prec, arith=arith,
-                                   sort_period=10, device=dev)
+                                   sort_period=10, device=dev, bin_slack=(float(fr), int(mn)))
             sim.load_species(0, init_uniform_device(geom, sp, dev, n0=0.0795774715,
                                                     precision=prec)[0])
             n = sim.particles[0].n
@@ -38,11 +42,12 @@ for n_target in (float(x) for x in args.sizes.split(",")):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             kern = 0.0
-            e0.record()
-            for _ in range(args.steps):
-                kern += sim.run_cycle().kernel_ms
-            e1.record()
-            torch.cuda.synchronize()
+            with ClockMonitor(torch.cuda.current_device()) as mon:
+                e0.record()
+                for _ in range(args.steps):
+                    kern += sim.run_cycle().kernel_ms
+                e1.record()
+                torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.steps
             bpp = 104 if mode == "double" else 52
             rate_k = n / (kern / args.steps * 1e-3)
@@ -51,6 +56,8 @@ for n_target in (float(x) for x in args.sizes.split(",")):
                               "particles_per_s_step": n / (ms * 1e-3),
                               "particles_per_s_kernel": rate_k,
                               "hbm_frac_kernel": rate_k * bpp / 1e9 / peak,
-                              "ms_per_step": ms}), flush=True)
+                              "ms_per_step": ms,
+                              "layout": "bins" if sim.binned else "flat",
+                              "clocks": mon.summary()}), flush=True)
             del sim
             torch.cuda.empty_cache()
