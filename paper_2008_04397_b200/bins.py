@@ -84,9 +84,10 @@ class BinnedSpecies:
         cap = int(total.value)
         self.cap = cap
         self.rec, self.ids = self._alloc_set(cap)
-        # the re-slack's destination, allocated now: a re-slack inside a run
-        # then only copies (no multi-GB allocation in the middle of a cycle)
-        self._spare = self._alloc_set(cap)
+        # the re-slack's destination: allocated after the first cycle (when the
+        # caller's flat input and the build's scratch are gone), so that a
+        # re-slack inside a run only copies
+        self._spare = None
         rc = L.bp_bins_fill(self.fbytes, *[_ptr(a) for a in parts.arrays()], _ptr(parts.ids),
                             parts.n, gf, gg, gi, _ptr(self.start), _ptr(self.rec), _ptr(self.ids),
                             ctypes.c_void_p(s.cuda_stream))
@@ -151,7 +152,7 @@ class BinnedSpecies:
         _lib.check(rc, "bins_reslack")
         cap = int(total.value)
         spare = self._spare
-        if spare[1].numel() < cap:
+        if spare is None or spare[1].numel() < cap:
             spare = self._alloc_set(cap)
         rc = L.bp_bins_reslack(*args, _ptr(spare[0]), _ptr(spare[1]), ctypes.byref(total),
                                ctypes.c_void_p(s.cuda_stream))
@@ -185,6 +186,8 @@ class BinnedSpecies:
         an overflow or a misplaced particle triggers a rebuild."""
         st = self.stats() if stats is None else stats
         self.last_stats = list(st)
+        if self._spare is None:
+            self._spare = self._alloc_set(self.cap)
         if st[STAT_LOST]:
             raise IntegrityError(f"{st[STAT_LOST]} particles lost: bin overflow / late list too "
                                  f"small (stats {st})")
