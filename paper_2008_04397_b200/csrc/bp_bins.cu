@@ -112,7 +112,7 @@ __device__ __forceinline__ void st_rec(float4* p, const float4& a, const float4&
                : "memory");
 }
 
-constexpr int kHoleCap = 64;     // leavers per bin per cycle tracked for the refill
+constexpr int kHoleCap = 256;    // leavers per bin per cycle tracked for the refill (more: misplaced, rebuild)
 constexpr int kMoveClaim = 8;    // bins per mover work claim
 constexpr int kLvChunk = 128;    // leaver slots per warp reservation
 constexpr int kDepClaim = 16;    // bins per deposit work claim (4 rounds of 4)
@@ -287,12 +287,14 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
                                                      const __grid_constant__ Bins b) {
   __shared__ __align__(128) float4 recs_s[kMoverWarps][2][kMoveClaim * 12];
   __shared__ __align__(8) unsigned long long bars_s[kMoverWarps][2];
-  __shared__ int holes_s[kMoverWarps][kHoleCap];
-  __shared__ long long lvslot_s[kMoverWarps][kHoleCap];
+  // hole slots within the bin (< 65536) and the leavers' list slots (< 2^31:
+  // the list holds a quarter of the species + 1M)
+  __shared__ unsigned short holes_s[kMoverWarps][kHoleCap];
+  __shared__ int lvslot_s[kMoverWarps][kHoleCap];
   const int wid = threadIdx.x >> 5;
   const unsigned lane = threadIdx.x & 31;
-  int* const holes = holes_s[wid];
-  long long* const lvslot = lvslot_s[wid];
+  unsigned short* const holes = holes_s[wid];
+  int* const lvslot = lvslot_s[wid];
   unsigned long long* const bars = bars_s[wid];
   const unsigned lt = lanemask_lt();
   const float qe = fabsf(a.qdt2m) * __ldg(a.emax) * 1.00001f;
@@ -418,15 +420,15 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
               rank < room ? lv_base + lv_used + rank : lv_next + (rank - room);
           // accepted leavers are a prefix in rank order (hole index grows
           // with the rank), so their hole indices stay contiguous
-          listed = leave && slot < b.lv_cap && nh + rank < kHoleCap;
+          listed = leave && slot < b.lv_cap && nh + rank < kHoleCap && r < 65536;
           if (listed) {
             // the id is added at the end of the bin (one load latency per
             // bin instead of per tile)
             float4* rec = reinterpret_cast<float4*>(b.lv + slot);
             rec[0] = make_float4(xp, yp, zp, un);
             rec[1] = make_float4(vn, wn, qp, __int_as_float(dest));
-            holes[nh + rank] = r;
-            lvslot[nh + rank] = slot;
+            holes[nh + rank] = (unsigned short)r;
+            lvslot[nh + rank] = (int)slot;
           } else if (leave) {
             // stays here as a misplaced particle (slow paths; host rebuilds)
             atomicAdd(&b.stat[ST_MISPLACED], 1ULL);
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           int nlow = 0;
           for (int k0 = 0; k0 < nh; k0 += 32) {
             const int k = k0 + (int)lane;
-            nlow += __popc(__ballot_sync(0xffffffffu, k < nh && holes[k] < n_stay));
+            nlow += __popc(__ballot_sync(0xffffffffu, k < nh && (int)holes[k] < n_stay));
           }
           for (int k0 = 0; k0 < nh; k0 += 32) {
             const int k = k0 + (int)lane;
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
             if (k < nlow) {
               int t = n_stay + k;
               for (int j = nlow; j < nh; ++j) {
-                if (holes[j] <= t) ++t;
+                if ((int)holes[j] <= t) ++t;
                 else break;
               }
               src = s0 + t;

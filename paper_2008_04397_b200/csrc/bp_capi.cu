@@ -728,6 +728,7 @@ int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int
   if (!rec || ((uintptr_t)rec % 16) != 0 || !records || ((uintptr_t)records % 32) != 0 ||
       !acc || !invvol || !ids || !start ||
       !count || !stat || !leavers || !overflow || !late || leaver_cap < 0 ||
+      leaver_cap > 0x7fffffffLL ||
       overflow_cap < 0 || late_cap < 0 ||
       n_iters < 0 || !d_status) {
     set_error("bins_cycle: bad arguments (records 32-byte aligned, buffers, d_status required)");
