@@ -181,15 +181,18 @@ __device__ __forceinline__ void load_record(const P& a, int cell, float4 (&R)[12
 // in another cell reloads it.  Every lane of the warp runs the whole push
 // (no early return: a failing particle keeps a safe position and reports
 // its status), so the reload is a warp-uniform branch.
-template <bool RX, bool RY, bool RZ>
+// NIT > 0: the iteration count as a compile-time constant (fully unrolled);
+// NIT == 0: a.n_iters at run time
+template <bool RX, bool RY, bool RZ, int NIT>
 __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, int home,
                                         const float4* home_rec, float& xp, float& yp,
                                         float& zp, float& un, float& vn, float& wn,
                                         bool skipbc) {
   float vbx = un, vby = vn, vbz = wn;
   int st = ST_OK;
-#pragma unroll 1
-  for (int it = 0; it < a.n_iters; ++it) {
+  const int nit = NIT > 0 ? NIT : a.n_iters;
+#pragma unroll
+  for (int it = 0; it < nit; ++it) {
     const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
     float xm = XM.x, ym = XM.y;
     float zm = fmaf(vbz, a.dth, zp);
@@ -282,7 +285,7 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 #endif
 constexpr int kMoverWarps = BP_MOVER_TPB / 32;
 
-template <bool RX, bool RY, bool RZ>
+template <bool RX, bool RY, bool RZ, int NIT>
 __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const __grid_constant__ P a,
                                                      const __grid_constant__ Bins b) {
   __shared__ __align__(128) float4 recs_s[kMoverWarps][2][kMoveClaim * 12];
@@ -387,7 +390,8 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           }
           const bool all_in =
               __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
-          const int st = push_bin<RX, RY, RZ>(a, R, held, c, rs, xp, yp, zp, un, vn, wn, all_in);
+          const int st =
+              push_bin<RX, RY, RZ, NIT>(a, R, held, c, rs, xp, yp, zp, un, vn, wn, all_in);
           int dest = c;
           if (st == ST_OK) {
             // the new cell (cell_of's formula, bp_f32_common.cuh)
@@ -901,7 +905,8 @@ int resident_grid(K k, size_t smem, int threads = 256) {
 
 template <bool RX, bool RY, bool RZ>
 int launch_mover_bins(const bins::P& a, const bins::Bins& b, cudaStream_t s) {
-  auto k = bins::mover_bins<RX, RY, RZ>;
+  // the reference's default of 3 midpoint iterations unrolled
+  auto k = a.n_iters == 3 ? bins::mover_bins<RX, RY, RZ, 3> : bins::mover_bins<RX, RY, RZ, 0>;
   const int g = resident_grid(k, 0, BP_MOVER_TPB);
   const int th = timing_begin(TK_MOVER, s);
   k<<<g, BP_MOVER_TPB, 0, s>>>(a, b);
