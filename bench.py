@@ -113,9 +113,9 @@ def peaks():
 
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
-    summary (profiles/ncu_summary_r02.json), or None."""
+    summary (profiles/ncu_summary_r02b.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary_r02.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary_r02b.json")) as f:
             return float(json.load(f)[kernel]["dram_bytes_per_launch"])
     except Exception:
         return None
