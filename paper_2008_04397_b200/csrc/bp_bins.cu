@@ -79,6 +79,8 @@ struct Bins {
   const long long* start;  // [ncell + 1]
   int* count;              // [ncell]
   int ncell;
+  int move_claim;  // bins per mover claim (<= kMoveClaim): small grids claim fewer
+  int dep_rounds;  // deposit rounds of 4 bins per claim (<= kDepClaim / 4)
   Leaver* lv;
   long long lv_cap;
   Leaver* ov;
@@ -113,9 +115,9 @@ __device__ __forceinline__ void st_rec(float4* p, const float4& a, const float4&
 }
 
 constexpr int kHoleCap = 256;    // leavers per bin per cycle tracked for the refill (more: misplaced, rebuild)
-constexpr int kMoveClaim = 8;    // bins per mover work claim
+constexpr int kMoveClaim = 8;    // bins per mover work claim (at most; Bins::move_claim)
 constexpr int kLvChunk = 128;    // leaver slots per warp reservation
-constexpr int kDepClaim = 16;    // bins per deposit work claim (4 rounds of 4)
+constexpr int kDepClaim = 16;    // bins per deposit work claim, 4 rounds of 4 (at most)
 constexpr int kRowS = 84;        // deposit transpose row stride (floats)
 constexpr int kWarpSm = 32 * kRowS + 32;
 
@@ -315,9 +317,9 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   auto claim = [&](int bf) -> int {
     unsigned long long c = 0;
     if (lane == 0) {
-      c = atomicAdd(&b.stat[ST_WORK_MOVE], (unsigned long long)kMoveClaim);
+      c = atomicAdd(&b.stat[ST_WORK_MOVE], (unsigned long long)b.move_claim);
       if (c < (unsigned long long)b.ncell) {
-        const int nb = min(kMoveClaim, b.ncell - (int)c);
+        const int nb = min(b.move_claim, b.ncell - (int)c);
         const unsigned bytes = (unsigned)nb * 12u * 16u;
         fence_proxy_async();
         mbar_expect_tx(&bars[bf], bytes);
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   };
   float4 R[12];
   while (c0 < b.ncell) {
-    const int c1 = min(c0 + kMoveClaim, b.ncell);
+    const int c1 = min(c0 + b.move_claim, b.ncell);
     const int cn = claim(bf ^ 1);  // the next claim's records load meanwhile
     mbar_wait(&bars[bf], phase[bf]);
     phase[bf] ^= 1u;
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
   };
   for (;;) {
     unsigned long long cc = 0;
-    if (lane == 0) cc = atomicAdd(&b.stat[ST_WORK_DEP], (unsigned long long)kDepClaim);
+    if (lane == 0) cc = atomicAdd(&b.stat[ST_WORK_DEP], (unsigned long long)(4 * b.dep_rounds));
     cc = __shfl_sync(0xffffffffu, cc, 0);
     if (cc >= (unsigned long long)b.ncell) break;
     const int c0 = (int)cc;
@@ -618,14 +620,14 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
     }
     fetch(s0 + l, l < n);
 #pragma unroll 1
-    for (int rnd = 0; rnd < kDepClaim / 4; ++rnd) {
+    for (int rnd = 0; rnd < b.dep_rounds; ++rnd) {
       if (c0 + 4 * rnd >= b.ncell) break;
       const bool okb = c < b.ncell;
       // next round's bin of this quarter
       const int cn = c + 4;
       long long s1 = 0;
       int n_1 = 0;
-      if (rnd + 1 < kDepClaim / 4 && cn < b.ncell) {
+      if (rnd + 1 < b.dep_rounds && cn < b.ncell) {
         s1 = b.start[cn];
         n_1 = (int)min((long long)b.count[cn], b.start[cn + 1] - s1);
       }
@@ -908,8 +910,13 @@ int launch_mover_bins(const bins::P& a, const bins::Bins& b, cudaStream_t s) {
   // the reference's default of 3 midpoint iterations unrolled
   auto k = a.n_iters == 3 ? bins::mover_bins<RX, RY, RZ, 3> : bins::mover_bins<RX, RY, RZ, 0>;
   const int g = resident_grid(k, 0, BP_MOVER_TPB);
+  // claims of up to 8 bins, fewer on small grids so that every warp gets
+  // several claims (the dynamic claiming then balances the tail)
+  bins::Bins bb = b;
+  const long long warps = (long long)g * (BP_MOVER_TPB / 32);
+  bb.move_claim = (int)std::max(1LL, std::min((long long)bins::kMoveClaim, b.ncell / (6 * warps)));
   const int th = timing_begin(TK_MOVER, s);
-  k<<<g, BP_MOVER_TPB, 0, s>>>(a, b);
+  k<<<g, BP_MOVER_TPB, 0, s>>>(a, bb);
   timing_end(th, s);
   note_launch();
   return bcheck("mover_bins launch");
@@ -965,6 +972,8 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
     cudaFuncSetAttribute(bins::deposit_bins, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   const int g = resident_grid(bins::deposit_bins, smem);
+  b.dep_rounds = (int)std::max(
+      1LL, std::min((long long)bins::kDepClaim / 4, (long long)b.ncell / (24LL * g * 8)));
   const int th = timing_begin(TK_DEPOSIT, s);
   bins::deposit_bins<<<g, 256, smem, s>>>(a, b);
   timing_end(th, s);
