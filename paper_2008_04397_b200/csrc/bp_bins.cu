@@ -584,8 +584,20 @@ __global__ void __launch_bounds__(256) deposit_list(const __grid_constant__ P a,
 // quarter's 8 rows (quarter offset 8q: the 32 lanes read 32 distinct banks).
 // The next particle of each lane (same bin, or the next round's bin) is
 // loaded while the current one is accumulated.
-__global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P a,
-                                                       const __grid_constant__ Bins b) {
+// measured (scripts/build_variants.sh): 4 particles per lane in flight at
+// 128 x 3 (12 warps, 168 registers) 0.53 ms; 1 at 256 x 2: 0.76 ms; 2: 0.69;
+// 3: 0.56; 6 or 8 spill
+#ifndef BP_DEP_TPB
+#define BP_DEP_TPB 128  // threads per block of deposit_bins
+#endif
+#ifndef BP_DEP_MINB
+#define BP_DEP_MINB 3
+#endif
+#ifndef BP_DEP_UNR
+#define BP_DEP_UNR 4    // particles per lane and iteration (loads in flight)
+#endif
+__global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __grid_constant__ P a,
+                                                                        const __grid_constant__ Bins b) {
   extern __shared__ __align__(16) float dsm[];
   const unsigned lane = threadIdx.x & 31;
   const int qd = (int)(lane >> 3), l = (int)(lane & 7);
@@ -593,14 +605,23 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
   float* const myrow = ws + lane * kRowS + 8 * qd;
   const float* const rd = ws + (8 * qd) * kRowS + 8 * qd + l;
   const int ci_off = l & 1, cj_off = (l >> 1) & 1, ck_off = (l >> 2) & 1;
-  float n1[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  auto fetch = [&](long long q, bool ok) {
-    if (ok) {
-      // read-only path (measured faster than streaming loads here)
-      float4 ra, rb;
-      ld_rec_ro(b.rec + 2 * q, ra, rb);
-      n1[0] = ra.x; n1[1] = ra.y; n1[2] = ra.z; n1[3] = ra.w;
-      n1[4] = rb.x; n1[5] = rb.y; n1[6] = rb.z;
+  constexpr int U = BP_DEP_UNR;
+  float n1[U][7];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int k = 0; k < 7; ++k) n1[u][k] = 0.f;
+  // the U particles q, q + 8, ... of this lane (those < lim): one 256-bit
+  // read-only load each
+  auto fetch = [&](long long q0, int i0, int lim) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (i0 + 8 * u < lim) {
+        float4 ra, rb;
+        ld_rec_ro(b.rec + 2 * (q0 + 8 * u), ra, rb);
+        n1[u][0] = ra.x; n1[u][1] = ra.y; n1[u][2] = ra.z; n1[u][3] = ra.w;
+        n1[u][4] = rb.x; n1[u][5] = rb.y; n1[u][6] = rb.z;
+      }
     }
   };
   for (;;) {
@@ -618,7 +639,7 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
       s0 = b.start[c];
       n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
     }
-    fetch(s0 + l, l < n);
+    fetch(s0 + l, l, n);
 #pragma unroll 1
     for (int rnd = 0; rnd < b.dep_rounds; ++rnd) {
       if (c0 + 4 * rnd >= b.ncell) break;
@@ -631,8 +652,9 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
         s1 = b.start[cn];
         n_1 = (int)min((long long)b.count[cn], b.start[cn + 1] - s1);
       }
-      const int nit = (int)__reduce_max_sync(0xffffffffu, (unsigned)((n + 7) >> 3));
-      if (nit == 0) fetch(s1 + l, l < n_1);  // (the loop below prefetches otherwise)
+      const int nit =
+          (int)__reduce_max_sync(0xffffffffu, (unsigned)((n + 8 * U - 1) / (8 * U)));
+      if (nit == 0) fetch(s1 + l, l, n_1);  // (the loop below prefetches otherwise)
       const Box bx = cell_box(a, q3);
       F2 A[10][4];
 #pragma unroll
@@ -641,49 +663,57 @@ __global__ void __launch_bounds__(256, 2) deposit_bins(const __grid_constant__ P
         for (int cp = 0; cp < 4; ++cp) A[k][cp] = f2(0.f, 0.f);
 #pragma unroll 1
       for (int it = 0; it < nit; ++it) {
-        const int pi = it * 8 + l;
-        bool valid = pi < n;
-        const float xp = n1[0], yp = n1[1], zp = n1[2], un = n1[3], vn = n1[4], wn = n1[5],
-                    qp = n1[6];
-        if (it + 1 < nit) fetch(s0 + pi + 8, pi + 8 < n);
-        else fetch(s1 + l, l < n_1);
-        const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
-        const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
-        const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
-        if (valid && !in_box(bx, gx, gy, gz)) {
-          // misplaced (a leaver the mover could not list): the late list
-          const unsigned long long o = atomicAdd(&b.stat[ST_LATE], 1ULL);
-          if ((long long)o < b.late_cap) {
-            Leaver L;
-            L.a = make_float4(xp, yp, zp, un);
-            L.b = make_float4(vn, wn, qp, 0.f);
-            L.id = 0;
-            L.pad = 0;
-            b.late[o] = L;
-          } else {
-            atomicAdd(&b.stat[ST_LOST], 1ULL);
+        const int pi = it * 8 * U + l;
+        float cur[U][7];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < 7; ++k) cur[u][k] = n1[u][k];
+        if (it + 1 < nit) fetch(s0 + pi + 8 * U, pi + 8 * U, n);
+        else fetch(s1 + l, l, n_1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bool valid = pi + 8 * u < n;
+          const float xp = cur[u][0], yp = cur[u][1], zp = cur[u][2], un = cur[u][3],
+                      vn = cur[u][4], wn = cur[u][5], qp = cur[u][6];
+          const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
+          const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
+          const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
+          if (valid && !in_box(bx, gx, gy, gz)) {
+            // misplaced (a leaver the mover could not list): the late list
+            const unsigned long long o = atomicAdd(&b.stat[ST_LATE], 1ULL);
+            if ((long long)o < b.late_cap) {
+              Leaver L;
+              L.a = make_float4(xp, yp, zp, un);
+              L.b = make_float4(vn, wn, qp, 0.f);
+              L.id = 0;
+              L.pad = 0;
+              b.late[o] = L;
+            } else {
+              atomicAdd(&b.stat[ST_LOST], 1ULL);
+            }
+            valid = false;
           }
-          valid = false;
+          const float qs = valid ? qp : 0.f;
+          const float fx = gx - bx.cf[0], fy = gy - bx.cf[1], fz = gz - bx.cf[2];
+          const F2 Q = f2(qs - qs * fx, qs * fx);  // q (1 - fx), q fx
+          const F2 Qy0 = __fmul2_rn(Q, f2(1.f - fy, 1.f - fy));
+          const F2 Qy1 = __fmul2_rn(Q, f2(fy, fy));
+          const float az = 1.f - fz;
+          F2 Bc[4];
+          Bc[0] = __fmul2_rn(Qy0, f2(az, az));
+          Bc[1] = __fmul2_rn(Qy1, f2(az, az));
+          Bc[2] = __fmul2_rn(Qy0, f2(fz, fz));
+          Bc[3] = __fmul2_rn(Qy1, f2(fz, fz));
+          const float mv[10] = {1.f,     un,      vn,      wn,      un * un,
+                                un * vn, un * wn, vn * vn, vn * wn, wn * wn};
+#pragma unroll
+          for (int cp = 0; cp < 4; ++cp) A[0][cp] = __fadd2_rn(A[0][cp], Bc[cp]);
+#pragma unroll
+          for (int k = 1; k < 10; ++k)
+#pragma unroll
+            for (int cp = 0; cp < 4; ++cp) A[k][cp] = fma2(Bc[cp], f2(mv[k], mv[k]), A[k][cp]);
         }
-        const float qs = valid ? qp : 0.f;
-        const float fx = gx - bx.cf[0], fy = gy - bx.cf[1], fz = gz - bx.cf[2];
-        const F2 Q = f2(qs - qs * fx, qs * fx);  // q (1 - fx), q fx
-        const F2 Qy0 = __fmul2_rn(Q, f2(1.f - fy, 1.f - fy));
-        const F2 Qy1 = __fmul2_rn(Q, f2(fy, fy));
-        const float az = 1.f - fz;
-        F2 Bc[4];
-        Bc[0] = __fmul2_rn(Qy0, f2(az, az));
-        Bc[1] = __fmul2_rn(Qy1, f2(az, az));
-        Bc[2] = __fmul2_rn(Qy0, f2(fz, fz));
-        Bc[3] = __fmul2_rn(Qy1, f2(fz, fz));
-        const float mv[10] = {1.f,     un,      vn,      wn,      un * un,
-                              un * vn, un * wn, vn * vn, vn * wn, wn * wn};
-#pragma unroll
-        for (int cp = 0; cp < 4; ++cp) A[0][cp] = __fadd2_rn(A[0][cp], Bc[cp]);
-#pragma unroll
-        for (int k = 1; k < 10; ++k)
-#pragma unroll
-          for (int cp = 0; cp < 4; ++cp) A[k][cp] = fma2(Bc[cp], f2(mv[k], mv[k]), A[k][cp]);
       }
       if (nit > 0) {
         // ---- flush: transpose through shared memory, then one corner per lane
@@ -966,16 +996,17 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   bins::migrate_bins<<<nsm() * 8, 256, 0, s>>>(b);
   note_launch();
   if ((rc = bcheck("migrate_bins launch"))) return rc;
-  const size_t smem = (size_t)8 * bins::kWarpSm * sizeof(float);
+  const size_t smem = (size_t)(BP_DEP_TPB / 32) * bins::kWarpSm * sizeof(float);
   static bool attr[64] = {};
   if (first_on_device(attr))
     cudaFuncSetAttribute(bins::deposit_bins, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  const int g = resident_grid(bins::deposit_bins, smem);
+  const int g = resident_grid(bins::deposit_bins, smem, BP_DEP_TPB);
   b.dep_rounds = (int)std::max(
-      1LL, std::min((long long)bins::kDepClaim / 4, (long long)b.ncell / (24LL * g * 8)));
+      1LL, std::min((long long)bins::kDepClaim / 4,
+                    (long long)b.ncell / (24LL * g * (BP_DEP_TPB / 32))));
   const int th = timing_begin(TK_DEPOSIT, s);
-  bins::deposit_bins<<<g, 256, smem, s>>>(a, b);
+  bins::deposit_bins<<<g, BP_DEP_TPB, smem, s>>>(a, b);
   timing_end(th, s);
   note_launch();
   if ((rc = bcheck("deposit_bins launch"))) return rc;
