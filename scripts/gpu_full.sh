@@ -17,5 +17,5 @@ if [ -z "$NOPROF" ]; then
 BP_TMA_STREAM=1 timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 \
     python scripts/debug/sanitize_driver.py > gpurun_out/sanitize_racecheck.txt 2>&1
 tail -2 gpurun_out/sanitize_racecheck.txt
-bash scripts/profile_r02.sh r02
+bash scripts/profile_r02.sh r02b
 fi

@@ -5,7 +5,7 @@
 #     device time and DRAM bytes, cold cache, serialised)
 #  2. full captures of the binned kernels (species 0, third step) and of the
 #     flat split kernels (species 0 at step 5 of the sort period)
-R=${1:-r02}
+R=${1:-r02b}
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches_$R.csv \
