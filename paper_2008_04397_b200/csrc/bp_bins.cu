@@ -183,12 +183,44 @@ __device__ __forceinline__ void load_record(const P& a, int cell, float4 (&R)[12
 // in another cell reloads it.  Every lane of the warp runs the whole push
 // (no early return: a failing particle keeps a safe position and reports
 // its status), so the reload is a warp-uniform branch.
+// The shared-memory field window of a mover claim of nb <= 8 bins along x
+// (cells c0 .. c0 + nb - 1 at (i0 .. i0 + nb - 1, j, k)): slots 0..9 the x
+// run c0 - 1 .. c0 + nb (the home records at 1 .. nb), 10..17 / 18..25 the
+// same x range at j - 1 / j + 1, 26..33 / 34..41 at k - 1 / k + 1, each
+// present when inside the grid (flags) — staged by TMA bulk copies, so a
+// midpoint that moved to a face neighbour reloads from shared memory.
+constexpr int kWinRecs = 10 + 4 * kMoveClaim;
+enum { WIN_XLO = 1, WIN_XHI = 2, WIN_YM = 4, WIN_YP = 8, WIN_ZM = 16, WIN_ZP = 32 };
+struct Win {
+  const float4* base;
+  int i0, j, k, nb, fl;
+};
+// window slot of cell (i, j, k), or -1 (global memory)
+__device__ __forceinline__ int win_slot(const Win& W, int i, int j, int k) {
+  const int di = i - W.i0;
+  if (j == W.j && k == W.k) {
+    if (di >= 0 && di < W.nb) return di + 1;
+    if (di == -1 && (W.fl & WIN_XLO)) return 0;
+    if (di == W.nb && (W.fl & WIN_XHI)) return W.nb + 1;
+    return -1;
+  }
+  if (di < 0 || di >= W.nb) return -1;
+  if (k == W.k) {
+    if (j == W.j - 1 && (W.fl & WIN_YM)) return 10 + di;
+    if (j == W.j + 1 && (W.fl & WIN_YP)) return 18 + di;
+  } else if (j == W.j) {
+    if (k == W.k - 1 && (W.fl & WIN_ZM)) return 26 + di;
+    if (k == W.k + 1 && (W.fl & WIN_ZP)) return 34 + di;
+  }
+  return -1;
+}
+
 // NIT > 0: the iteration count as a compile-time constant (fully unrolled);
 // NIT == 0: a.n_iters at run time
 template <bool RX, bool RY, bool RZ, int NIT>
 __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, int home,
-                                        const float4* home_rec, float& xp, float& yp,
-                                        float& zp, float& un, float& vn, float& wn,
+                                        const float4* home_rec, const Win& W, float& xp,
+                                        float& yp, float& zp, float& un, float& vn, float& wn,
                                         bool skipbc) {
   float vbx = un, vby = vn, vbz = wn;
   int st = ST_OK;
@@ -220,7 +252,17 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
 #pragma unroll
           for (int q = 0; q < 12; ++q) R[q] = home_rec[q];
         } else {
+#if BP_MOVER_WINDOW
+          const int sl = win_slot(W, i, j, k);
+          if (sl >= 0) {
+#pragma unroll
+            for (int q = 0; q < 12; ++q) R[q] = W.base[sl * 12 + q];
+          } else {
+            load_record(a, cell, R);
+          }
+#else
           load_record(a, cell, R);
+#endif
         }
       }
     }
@@ -279,6 +321,9 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 // the holes below the new count are refilled with the bin's trailing stayers
 // (about as many particle copies as leavers).  The next tile's particles
 // (across bins of the claim) are loaded while the current tile is pushed.
+#ifndef BP_MOVER_WINDOW
+#define BP_MOVER_WINDOW 0  // 1: face-neighbour field window staged per claim
+#endif
 #ifndef BP_MOVER_TPB
 #define BP_MOVER_TPB 128  // threads per block of mover_bins (measured: 128 x 5 > 256 x 2)
 #endif
@@ -290,7 +335,11 @@ constexpr int kMoverWarps = BP_MOVER_TPB / 32;
 template <bool RX, bool RY, bool RZ, int NIT>
 __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const __grid_constant__ P a,
                                                      const __grid_constant__ Bins b) {
+#if BP_MOVER_WINDOW
+  __shared__ __align__(128) float4 win_s[kMoverWarps][kWinRecs * 12];
+#else
   __shared__ __align__(128) float4 recs_s[kMoverWarps][2][kMoveClaim * 12];
+#endif
   __shared__ __align__(8) unsigned long long bars_s[kMoverWarps][2];
   // hole slots within the bin (< 65536) and the leavers' list slots (< 2^31:
   // the list holds a quarter of the species + 1M)
@@ -313,6 +362,49 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   }
   fence_proxy_async();
   __syncwarp();
+#if BP_MOVER_WINDOW
+  // claim up to 8 bins and stage their field window (single buffer: the
+  // next claim's copies start when this claim is done)
+  Win W{win_s[wid], 0, 0, 0, 0, 0};
+  auto claim_win = [&]() -> int {
+    unsigned long long cc = 0;
+    if (lane == 0) cc = atomicAdd(&b.stat[ST_WORK_MOVE], (unsigned long long)b.move_claim);
+    const int c = (int)min(__shfl_sync(0xffffffffu, cc, 0), (unsigned long long)b.ncell);
+    if (c >= b.ncell) return c;
+    const int nb = min(b.move_claim, b.ncell - c);
+    W.i0 = c % a.nx;
+    W.j = (c / a.nx) % a.ny;
+    W.k = c / a.cny;
+    W.nb = nb;
+    // a claim crossing an x row stages its home records only
+    const bool row = W.i0 + nb <= a.nx;
+    W.fl = row ? ((W.i0 > 0 ? WIN_XLO : 0) | (W.i0 + nb < a.nx ? WIN_XHI : 0) |
+                  (W.j > 0 ? WIN_YM : 0) | (W.j < a.ny - 1 ? WIN_YP : 0) |
+                  (W.k > 0 ? WIN_ZM : 0) | (W.k < a.nz - 1 ? WIN_ZP : 0))
+               : 0;
+    if (!row) W.i0 = -1000;  // no cell matches the window geometry
+    if (lane == 0) {
+      const unsigned rb = 12u * 16u;
+      const int xa = (W.fl & WIN_XLO) ? c - 1 : c;
+      const int xb = (W.fl & WIN_XHI) ? c + nb : c + nb - 1;
+      unsigned bytes = (unsigned)(xb - xa + 1) * rb;
+      const int runs[4] = {c - a.nx, c + a.nx, c - a.cny, c + a.cny};
+      const int rfl[4] = {WIN_YM, WIN_YP, WIN_ZM, WIN_ZP};
+      for (int q = 0; q < 4; ++q)
+        if (W.fl & rfl[q]) bytes += (unsigned)nb * rb;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[0], bytes);
+      bulk_load(win_s[wid] + (xa - (c - 1)) * 12, rec_g + (size_t)xa * 12,
+                (unsigned)(xb - xa + 1) * rb, &bars[0]);
+      for (int q = 0; q < 4; ++q)
+        if (W.fl & rfl[q])
+          bulk_load(win_s[wid] + (10 + 8 * q) * 12, rec_g + (size_t)runs[q] * 12,
+                    (unsigned)nb * rb, &bars[0]);
+    }
+    return c;
+  };
+#else
+  const Win W{nullptr, 0, 0, 0, 0, 0};  // (unused)
   // claim kMoveClaim bins and stage their records into buffer `bf`
   auto claim = [&](int bf) -> int {
     unsigned long long c = 0;
@@ -328,13 +420,18 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
     }
     return (int)min(__shfl_sync(0xffffffffu, c, 0), (unsigned long long)b.ncell);
   };
+#endif
   // the warp's current chunk of leaver slots [lv_base, lv_base + kLvChunk),
   // lv_used of them taken (starts "full": the first leaver claims a chunk)
   long long lv_base = 0, lv_next = 0;
   int lv_used = kLvChunk;
   unsigned phase[2] = {0u, 0u};
   int bf = 0;
+#if BP_MOVER_WINDOW
+  int c0 = claim_win();
+#else
   int c0 = claim(0);
+#endif
   // prefetched particle (one per lane) and the slot it came from
   float4 n1a = make_float4(0.f, 0.f, 0.f, 0.f), n1b = n1a;
   auto fetch = [&](long long q, bool ok) {
@@ -346,9 +443,14 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   float4 R[12];
   while (c0 < b.ncell) {
     const int c1 = min(c0 + b.move_claim, b.ncell);
+#if BP_MOVER_WINDOW
+    mbar_wait(&bars[0], phase[0]);
+    phase[0] ^= 1u;
+#else
     const int cn = claim(bf ^ 1);  // the next claim's records load meanwhile
     mbar_wait(&bars[bf], phase[bf]);
     phase[bf] ^= 1u;
+#endif
     long long s0 = b.start[c0];
     int n = (int)min((long long)b.count[c0], b.start[c0 + 1] - s0);
     fetch(s0 + lane, (int)lane < n);
@@ -365,7 +467,11 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
       }
       if (n > 0) {
         if (!pf_ok) fetch(s0 + lane, (int)lane < n);
+#if BP_MOVER_WINDOW
+        const float4* rs = win_s[wid] + (1 + c - c0) * 12;
+#else
         const float4* rs = recs_s[wid][bf] + (c - c0) * 12;
+#endif
 #pragma unroll
         for (int q = 0; q < 12; ++q) R[q] = rs[q];
         const float vmax = bin_speed_bound(a, q3, qe, hmin, epsmax);
@@ -393,7 +499,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           const bool all_in =
               __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
           const int st =
-              push_bin<RX, RY, RZ, NIT>(a, R, held, c, rs, xp, yp, zp, un, vn, wn, all_in);
+              push_bin<RX, RY, RZ, NIT>(a, R, held, c, rs, W, xp, yp, zp, un, vn, wn, all_in);
           int dest = c;
           if (st == ST_OK) {
             // the new cell (cell_of's formula, bp_f32_common.cuh)
@@ -506,8 +612,12 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
       n = n_1;
     }
     __syncwarp();  // every lane is done with buffer bf before it is refilled
+#if BP_MOVER_WINDOW
+    c0 = claim_win();
+#else
     c0 = cn;
     bf ^= 1;
+#endif
   }
   // unused slots of the last leaver chunk carry no particle
   for (int k = lv_used + (int)lane; k < kLvChunk; k += 32)
