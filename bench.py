@@ -122,18 +122,64 @@ def ncu_traffic(kernel):
 
 
 class ClockMonitor:
-    """nvidia-smi sampling of SM clock and throttle reasons during the timed
-    region (the profiling recipe's clocks line)."""
+    """SM clock, power and throttle reasons sampled during the timed region
+    (the profiling recipe's clocks line): NVML polled every 2 ms from a
+    thread (short timed regions, e.g. 20 steps at 8 GPUs, still get
+    samples; one sample is taken at entry and one at exit), else
+    nvidia-smi -lms 50."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.rows = []
+
+    def _nvml_handle(self, nv):
+        try:  # the CUDA device's own PCI address (CUDA and NVML orders can differ)
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self, nv, h):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        self.rows.append((float(sm), float(mx), pw,
+                          ["Active" if rs & b else "Not Active" for b in bits]))
 
     def __enter__(self):
+        import threading
+        self.rows = []
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = self._nvml_handle(nv)
+            self._nv, self._h = nv, h
+            self._stop = threading.Event()
+            self._sample(nv, h)
+
+            def poll():
+                while not self._stop.wait(0.002):
+                    try:
+                        self._sample(nv, h)
+                    except Exception:
+                        return
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -144,7 +190,14 @@ class ClockMonitor:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=5)
+            try:
+                self._sample(self._nv, self._h)
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -152,22 +205,22 @@ class ClockMonitor:
             except Exception:
                 self.proc.kill()
                 out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            for ln in out.splitlines():
+                p = [x.strip() for x in ln.split(",")]
+                try:
+                    self.rows.append((float(p[0]), float(p[1]), float(p[2]), p[3:7]))
+                except Exception:
+                    continue
 
     def summary(self):
-        rows = []
-        for ln in getattr(self, "lines", []):
-            p = [x.strip() for x in ln.split(",")]
-            try:
-                rows.append((float(p[0]), float(p[1]), float(p[2]), p[3:7]))
-            except Exception:
-                continue
+        rows = self.rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({n for r in rows for n, v in zip(names, r[3]) if v.lower() == "active"})
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[3])
+                          if v.lower() == "active"})
         return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1],
                 "power_w_max": max(r[2] for r in rows), "samples": len(rows),
+                "source": "nvml" if self.thread is not None else "nvidia-smi",
                 "reasons": reasons}
 
 
