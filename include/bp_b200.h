@@ -224,7 +224,8 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  *                into acc (+=); leavers / overflow / late are lists of
  *                bp_bins_leaver_bytes() records (the leaver list is scratch
  *                of the call, the overflow list feeds the rebuild, the late
- *                list holds misplaced particles met by the deposit), with
+ *                list holds misplaced particles met by the deposit; it may alias the
+ *                leaver list, which the migration has drained by then), with
  *                the per-cell records of
  *                bp_field_records_build (pbytes 4); asynchronous; the worst
  *                particle status goes to *d_status (atomicMax).  stat[8]

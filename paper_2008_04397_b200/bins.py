@@ -58,9 +58,6 @@ class BinnedSpecies:
         rb = int(_lib.load().bp_bins_leaver_bytes())
         self.overflow_cap = max(4096, int(parts.n * overflow_frac))
         self.overflow = torch.empty(self.overflow_cap * rb, dtype=torch.uint8, device=dev)
-        # misplaced particles the deposit meets (deposited on their own)
-        self.late_cap = max(4096, int(parts.n * overflow_frac))
-        self.late = torch.empty(self.late_cap * rb, dtype=torch.uint8, device=dev)
         self.rebuilds = 0
         self.last_stats = None
         self._build(parts, stream)
@@ -168,13 +165,17 @@ class BinnedSpecies:
 
     # ------------------------------------------------------------ cycle
     def cycle(self, lists, records, acc, invvol, sc, n_iters, scale, d_status, stream):
-        """Mover + migration + deposit of this species (asynchronous)."""
+        """Mover + migration + deposit of this species (asynchronous, on
+        `stream`, which must be the stream `lists` is used on)."""
         L = _lib.load()
         gf, gg, gi = (ctypes.c_void_p(x.ctypes.data) for x in (self.geo_f, self.geo_g, self.geo_i))
         rc = L.bp_bins_cycle(self.fbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start),
                              _ptr(self.count), self.ncell, _ptr(lists.leavers), lists.leaver_cap,
-                             _ptr(self.overflow), self.overflow_cap, _ptr(self.late),
-                             self.late_cap, _ptr(self.stat),
+                             _ptr(self.overflow), self.overflow_cap,
+                             # the late list (misplaced particles the deposit
+                             # meets) reuses the leaver list: the migration
+                             # drained it before the deposit runs
+                             _ptr(lists.leavers), lists.slots, _ptr(self.stat),
                              ctypes.c_void_p(records), _ptr(acc), _ptr(invvol), gf, gg, gi,
                              float(sc["dt"]), float(sc["dth"]), float(sc["qdt2m"]),
                              float(sc["beta"]), float(sc["one"]), int(n_iters), float(scale),
@@ -203,7 +204,8 @@ class BinnedSpecies:
 class TransitLists:
     """The leaver list shared by the species of a simulation: filled by one
     species' mover and drained by its migration, inside one bp_bins_cycle on
-    one stream (species on other streams need their own)."""
+    one stream (species on other streams need their own); the deposit then
+    reuses it as the late list."""
 
     def __init__(self, device, n_max, leaver_frac=0.25):
         import torch
@@ -211,3 +213,5 @@ class TransitLists:
         # + the warps' partly used 128-slot chunks (bp_bins.cu kLvChunk)
         self.leaver_cap = int(n_max * leaver_frac) + (1 << 20)
         self.leavers = torch.empty(self.leaver_cap * rb, dtype=torch.uint8, device=device)
+        # the buffer's records: the late list's capacity
+        self.slots = self.leaver_cap
