@@ -200,20 +200,22 @@ int bp_susceptibility(const int64_t* const* rho_rows, const double* qom, int nsp
 int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void* stream);
 
 /* ------------------------------------------------------------------------
- * Cell-binned layout (f32 particles, fast arithmetic) — the device-resident
- * cycle path (pipeline.DeviceSimulation layout "bins").  It replaces the
+ * Cell-binned layout (fast arithmetic; f32 particles with f32 or f64 fields,
+ * or f64 particles with f64 fields) — the device-resident cycle path
+ * (pipeline.DeviceSimulation layout "bins").  It replaces the
  * reference's phase 3 + phase 6 pair, run_cycle's per-batch fused_span calls
  * (pipeline.py:178-268, kernels.py:458-735) and the periodic stable cell sort
  * (pipeline.py:300-304, particles.py:157-167), for one species at a time:
- * the particles are 32-byte records (float x y z u | v w q 0, 16-byte
- * aligned; rec) with an int64 id array; cell c owns slots [start[c],
+ * the particles are records of 8 scalars of pbytes each (x y z u | v w q 0:
+ * 32 bytes for f32, 64 for f64; 32-byte aligned; rec) with an int64 id
+ * array; cell c owns slots [start[c],
  * start[c+1]), the first count[c] live; every bp_bins_cycle leaves each
  * particle in its cell's bin, so the order is cell-sorted every cycle.
  * Records, ids, start, count, the leaver / overflow lists, stat, field
  * records, acc, invvol: DEVICE pointers.
  *
- * bp_bins_plan   histogram of the flat arrays' cells (the fast kernels' f32
- *                cell formula) into count[ncell]; start[ncell + 1] = exclusive
+ * bp_bins_plan   histogram of the flat arrays' cells (the fast kernels' cell
+ *                formula in the particle precision) into count[ncell]; start[ncell + 1] = exclusive
  *                scan of count + max(slack_min, ceil(slack_frac * count));
  *                *total = start[ncell] (host int64; the call synchronises).
  *                Returns 3 (BP_ERR_DOMAIN) for positions below the origin.
@@ -222,12 +224,15 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  *                (synchronises).
  * bp_bins_cycle  mover + leaver migration + 10-moment deposit of the bins
  *                into acc (+=); leavers / overflow / late are lists of
- *                bp_bins_leaver_bytes() records (the leaver list is scratch
+ *                bp_bins_leaver_bytes(pbytes) records (the leaver list is scratch
  *                of the call, the overflow list feeds the rebuild, the late
  *                list holds misplaced particles met by the deposit; it may alias the
  *                leaver list, which the migration has drained by then), with
- *                the per-cell records of
- *                bp_field_records_build (pbytes 4); asynchronous; the worst
+ *                `records` = for f32 particles the per-cell records of
+ *                bp_field_records_build (pbytes 4), for f64 particles the
+ *                node records of bp_node_records_build (pbytes 8) — the f64
+ *                cycle is bitwise the flat f64 fast path's (particles and
+ *                lattice); asynchronous; the worst
  *                particle status goes to *d_status (atomicMax).  stat[8]
  *                (uint64) counts leavers (0), overflowed leavers (1),
  *                misplaced particles (2) and lost particles (3): after the
@@ -250,16 +255,16 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
 #define BP_BINS_STAT_OVERFLOW 1
 #define BP_BINS_STAT_MISPLACED 2
 #define BP_BINS_STAT_LOST 3
-int bp_bins_leaver_bytes(void);
-int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+int bp_bins_leaver_bytes(int pbytes);
+int bp_bins_plan(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
                  double slack_frac, int slack_min, int32_t* count, int64_t* start,
                  int64_t* total, void* stream);
-int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
+int bp_bins_fill(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
                  const void* vs, const void* ws, const void* qs, const int64_t* ids, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
                  const int64_t* start, void* dst_rec, int64_t* dst_ids, void* stream);
-int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_cycle(int pbytes, int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                   int64_t ncell,
                   void* leavers, int64_t leaver_cap, void* overflow, int64_t overflow_cap,
                   void* late, int64_t late_cap, uint64_t* stat, const void* records,
@@ -267,14 +272,23 @@ int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int
                   const double* geo_f, const double* geo_g, const int64_t* geo_i, double dt,
                   double dth, double qdt2m, double beta, double one, int n_iters, double scale,
                   int* d_status, void* stream);
-int bp_bins_reslack(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_reslack(int pbytes, const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                     int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                     double slack_frac, int slack_min, int32_t* new_count, int64_t* new_start,
                     void* dst_rec, int64_t* dst_ids, int64_t* total, void* stream);
-int bp_bins_export(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_export(int pbytes, const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream);
+
+/* Node records of the generic fast arithmetic (f64 binned cycle): Ex Ey Ez
+ * Bx By Bz invvol 0 per node in the particle precision (pbytes), then max
+ * |invvol| (f64) in the last 32 bytes; bp_node_records_bytes() gives the
+ * size of the (32-byte aligned) device buffer.  Asynchronous. */
+int64_t bp_node_records_bytes(int pbytes, const int64_t* geo_i);
+int bp_node_records_build(int pbytes, int fbytes, const void* E, const void* B,
+                          const void* invvol, const int64_t* geo_i, void* records,
+                          void* stream);
 
 /* ------------------------------------------------------------------------
  * Bit-exact device loader: one species of the reference's init_maxwellian

@@ -1,11 +1,12 @@
-"""Cell-binned device layout of one species (csrc/bp_bins.cu, C ABI
-``bp_bins_*``): the f32 fast path of :class:`pipeline.DeviceSimulation`.
+"""Cell-binned device layout of one species (csrc/bp_bins.cu for f32
+particles, csrc/bp_bins64.cu for f64; C ABI ``bp_bins_*``): the fast-arithmetic
+layout of :class:`pipeline.DeviceSimulation`.
 
 The reference restores cell order with a stable sort every ``sort_period``
 cycles (particles.py:157-167, pipeline.py:300-304).  Here cell ``c`` owns
-slots ``[start[c], start[c + 1])`` of 32-byte particle records (the
-reference's ParticleBuffer columns x y z u v w q_p, then 0) and of the int64
-ids, the first
+slots ``[start[c], start[c + 1])`` of particle records (the reference's
+ParticleBuffer columns x y z u v w q_p, then 0: 32 bytes in f32, 64 in f64)
+and of the int64 ids, the first
 ``count[c]`` of them live, and every cycle (``bp_bins_cycle``: mover, leaver
 migration, deposit) leaves each particle in its cell's bin — cell-sorted at
 every cycle.  ``flat()`` exports the live particles (cell order) as a
@@ -36,9 +37,13 @@ class BinnedSpecies:
     def __init__(self, parts, geom, geo_f, geo_g, geo_i, fbytes, slack=(0.5, 64),
                  overflow_frac=1.0 / 16, stream=None):
         import torch
-        if parts.dtype != torch.float32:
-            raise TypeError("the binned layout holds f32 particles")
+        if parts.dtype not in (torch.float32, torch.float64):
+            raise TypeError("the binned layout holds f32 or f64 particles")
+        if parts.dtype == torch.float64 and int(fbytes) != 8:
+            raise TypeError("f64 particles need f64 fields")
         self.torch = torch
+        self.dtype = parts.dtype
+        self.pbytes = parts.x.element_size()
         self.geom = geom
         self.geo_f = np.ascontiguousarray(geo_f, np.float64)
         self.geo_g = np.ascontiguousarray(geo_g, np.float64)
@@ -55,7 +60,7 @@ class BinnedSpecies:
         self.stat = torch.zeros(8, dtype=torch.int64, device=dev)
         # this species' overflow list: leavers whose bin was full (deposited
         # on their own, merged back by the rebuild after the cycle)
-        rb = int(_lib.load().bp_bins_leaver_bytes())
+        rb = int(_lib.load().bp_bins_leaver_bytes(self.pbytes))
         self.overflow_cap = max(4096, int(parts.n * overflow_frac))
         self.overflow = torch.empty(self.overflow_cap * rb, dtype=torch.uint8, device=dev)
         self.rebuilds = 0
@@ -72,7 +77,7 @@ class BinnedSpecies:
         s = self._stream(stream)
         total = ctypes.c_int64(0)
         gf, gg, gi = (ctypes.c_void_p(a.ctypes.data) for a in (self.geo_f, self.geo_g, self.geo_i))
-        rc = L.bp_bins_plan(self.fbytes, _ptr(parts.x), _ptr(parts.y), _ptr(parts.z), parts.n,
+        rc = L.bp_bins_plan(self.pbytes, self.fbytes, _ptr(parts.x), _ptr(parts.y), _ptr(parts.z), parts.n,
                             gf, gg, gi, self.slack[0], self.slack[1], _ptr(self.count),
                             _ptr(self.start), ctypes.byref(total), ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_plan")
@@ -85,19 +90,20 @@ class BinnedSpecies:
         # caller's flat input and the build's scratch are gone), so that a
         # re-slack inside a run only copies
         self._spare = None
-        rc = L.bp_bins_fill(self.fbytes, *[_ptr(a) for a in parts.arrays()], _ptr(parts.ids),
+        rc = L.bp_bins_fill(self.pbytes, self.fbytes, *[_ptr(a) for a in parts.arrays()],
+                            _ptr(parts.ids),
                             parts.n, gf, gg, gi, _ptr(self.start), _ptr(self.rec), _ptr(self.ids),
                             ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_fill")
         self.n = parts.n
 
     def _alloc_set(self, cap):
-        """One buffer set (32-byte records x y z u | v w q 0, int64 ids) for
-        `cap` slots plus headroom (3% + 64k slots), so that the slightly
-        larger layouts of later re-slacks fit."""
+        """One buffer set (records x y z u | v w q 0 of the particle dtype,
+        int64 ids) for `cap` slots plus headroom (3% + 64k slots), so that the
+        slightly larger layouts of later re-slacks fit."""
         torch = self.torch
         n = int(cap * 1.03) + (1 << 16)
-        return (torch.empty(8 * n, dtype=torch.float32, device=self.device),
+        return (torch.empty(8 * n, dtype=self.dtype, device=self.device),
                 torch.empty(n, dtype=torch.int64, device=self.device))
 
     def flat(self, stream=None):
@@ -108,13 +114,13 @@ class BinnedSpecies:
         s = self._stream(stream)
         off = torch.empty(self.ncell + 1, dtype=torch.int64, device=self.device)
         total = ctypes.c_int64(0)
-        args = (_ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
-                _ptr(self.overflow), self.overflow_cap, _ptr(self.stat))
+        args = (self.pbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count),
+                self.ncell, _ptr(self.overflow), self.overflow_cap, _ptr(self.stat))
         rc = L.bp_bins_export(*args, _ptr(off), None, None, ctypes.byref(total),
                               ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_export")
         n = int(total.value)
-        out = [torch.empty(n, dtype=torch.float32, device=self.device) for _ in ARRAYS]
+        out = [torch.empty(n, dtype=self.dtype, device=self.device) for _ in ARRAYS]
         ids = torch.empty(n, dtype=torch.int64, device=self.device)
         if n:
             dst = (ctypes.c_void_p * 7)(*[a.data_ptr() for a in out])
@@ -141,9 +147,9 @@ class BinnedSpecies:
         ncount = torch.empty(self.ncell, dtype=torch.int32, device=self.device)
         nstart = torch.empty(self.ncell + 1, dtype=torch.int64, device=self.device)
         total = ctypes.c_int64(0)
-        args = (_ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count), self.ncell,
-                _ptr(self.overflow), self.overflow_cap, _ptr(self.stat), self.slack[0],
-                self.slack[1], _ptr(ncount), _ptr(nstart))
+        args = (self.pbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start), _ptr(self.count),
+                self.ncell, _ptr(self.overflow), self.overflow_cap, _ptr(self.stat),
+                self.slack[0], self.slack[1], _ptr(ncount), _ptr(nstart))
         rc = L.bp_bins_reslack(*args, None, None, ctypes.byref(total),
                                ctypes.c_void_p(s.cuda_stream))
         _lib.check(rc, "bins_reslack")
@@ -169,7 +175,7 @@ class BinnedSpecies:
         `stream`, which must be the stream `lists` is used on)."""
         L = _lib.load()
         gf, gg, gi = (ctypes.c_void_p(x.ctypes.data) for x in (self.geo_f, self.geo_g, self.geo_i))
-        rc = L.bp_bins_cycle(self.fbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start),
+        rc = L.bp_bins_cycle(self.pbytes, self.fbytes, _ptr(self.rec), _ptr(self.ids), _ptr(self.start),
                              _ptr(self.count), self.ncell, _ptr(lists.leavers), lists.leaver_cap,
                              _ptr(self.overflow), self.overflow_cap,
                              # the late list (misplaced particles the deposit
@@ -207,9 +213,10 @@ class TransitLists:
     one stream (species on other streams need their own); the deposit then
     reuses it as the late list."""
 
-    def __init__(self, device, n_max, leaver_frac=0.25):
+    def __init__(self, device, n_max, leaver_frac=0.25, pbytes=4):
         import torch
-        rb = int(_lib.load().bp_bins_leaver_bytes())
+        self.pbytes = int(pbytes)
+        rb = int(_lib.load().bp_bins_leaver_bytes(self.pbytes))
         # + the warps' partly used 128-slot chunks (bp_bins.cu kLvChunk)
         self.leaver_cap = int(n_max * leaver_frac) + (1 << 20)
         self.leavers = torch.empty(self.leaver_cap * rb, dtype=torch.uint8, device=device)

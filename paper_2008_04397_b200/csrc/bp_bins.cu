@@ -44,6 +44,7 @@
 #include <cstdio>
 
 #include "bp_f32_common.cuh"
+#include "bp_bins_plumb.cuh"
 #include "bp_launch.h"
 
 namespace bp {
@@ -54,41 +55,8 @@ using sk::f2;
 using sk::fma2;
 typedef sk::Params<float> P;
 
-// a leaver in transit: 48 bytes
-struct __align__(16) Leaver {
-  float4 a;  // x y z u
-  float4 b;  // v w q, destination cell (int bits; < 0: no particle)
-  long long id;
-  long long pad;
-};
-
-enum {
-  ST_LEAVERS = 0,    // leaver slots claimed this cycle
-  ST_OVERFLOW = 1,   // leavers that found their bin full
-  ST_MISPLACED = 2,  // particles left in a bin that is not their cell
-  ST_LOST = 3,       // overflow list full: particles dropped (fatal)
-  ST_WORK_MOVE = 4,  // work counters
-  ST_WORK_DEP = 5,
-  ST_LATE = 6,       // misplaced particles the deposit listed for deposit_list
-  ST_N = 8
-};
-
-struct Bins {
-  float4* rec;  // 2 per slot: x y z u | v w q 0 (32-byte particle records)
-  long long* id;
-  const long long* start;  // [ncell + 1]
-  int* count;              // [ncell]
-  int ncell;
-  int move_claim;  // bins per mover claim (<= kMoveClaim): small grids claim fewer
-  int dep_rounds;  // deposit rounds of 4 bins per claim (<= kDepClaim / 4)
-  Leaver* lv;
-  long long lv_cap;
-  Leaver* ov;
-  long long ov_cap;
-  Leaver* late;  // the deposit's misplaced particles (deposited by deposit_list)
-  long long late_cap;
-  unsigned long long* stat;  // [ST_N]
-};
+typedef BinsT<float> Bins;
+typedef LeaverT<float> Leaver;
 
 // one 32-byte particle record per thread: a single 256-bit access (sm_100
 // ld/st .v8), so the lanes of a warp cover whole sectors with one instruction
@@ -108,12 +76,6 @@ __device__ __forceinline__ void st_rec_stream(float4* p, const float4& a, const 
                "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
                : "memory");
 }
-__device__ __forceinline__ void st_rec(float4* p, const float4& a, const float4& b) {
-  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x),
-               "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
-               : "memory");
-}
-
 constexpr int kHoleCap = 256;    // leavers per bin per cycle tracked for the refill (more: misplaced, rebuild)
 constexpr int kMoveClaim = 8;    // bins per mover work claim (at most; Bins::move_claim)
 constexpr int kLvChunk = 128;    // leaver slots per warp reservation
@@ -625,30 +587,6 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 }
 
 // ---------------------------------------------------------------------------
-// Migration: every listed leaver claims a slot at the end of its new bin.
-__global__ void __launch_bounds__(256) migrate_bins(const __grid_constant__ Bins b) {
-  const long long nl = min((long long)b.stat[ST_LEAVERS], b.lv_cap);
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
-    const Leaver L = b.lv[i];
-    const int dest = __float_as_int(L.b.w);
-    if (dest < 0 || dest >= b.ncell) continue;
-    const int pos = atomicAdd(&b.count[dest], 1);
-    const long long s = b.start[dest];
-    if (pos < b.start[dest + 1] - s) {
-      const long long d = s + pos;
-      // one full 32-byte sector (no partial-sector read-modify-write)
-      st_rec(b.rec + 2 * d, L.a, make_float4(L.b.x, L.b.y, L.b.z, 0.f));
-      b.id[d] = L.id;
-    } else {
-      const unsigned long long o = atomicAdd(&b.stat[ST_OVERFLOW], 1ULL);
-      if ((long long)o < b.ov_cap) b.ov[o] = L;
-      else atomicAdd(&b.stat[ST_LOST], 1ULL);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Deposit of the overflow list and of the particles the deposit found
 // misplaced: one particle straight onto the lattice with the reference's
 // per-contribution rounding (kernels.py:689-734).  Rare.
@@ -864,157 +802,6 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
   }
 }
 
-// ---------------------------------------------------------------------------
-// Build: fast-f32 cell keys (cell_of), histogram, capacities, stable scatter.
-__global__ void bin_keys(const P a, const float* __restrict__ x, const float* __restrict__ y,
-                         const float* __restrict__ z, long long n, unsigned* keys,
-                         unsigned* idx, int* hist, int* bad) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
-    const float gx = fmaf(x[p], a.idx[0], -a.ogs[0]);
-    const float gy = fmaf(y[p], a.idx[1], -a.ogs[1]);
-    const float gz = fmaf(z[p], a.idx[2], -a.ogs[2]);
-    int c = 0;
-    if (!(gx > -1.f && gy > -1.f && gz > -1.f)) {
-      *bad = 1;
-    } else {
-      const int i = min((int)gx, a.nx - 1), j = min((int)gy, a.ny - 1),
-                k = min((int)gz, a.nz - 1);
-      c = i + a.nx * j + a.cny * k;
-    }
-    if (keys) keys[p] = (unsigned)c;
-    if (idx) idx[p] = (unsigned)p;
-    if (hist) atomicAdd(hist + c, 1);
-  }
-}
-
-__global__ void bin_caps(const int* __restrict__ cnt, int ncell, float frac, int smin,
-                         long long* cap) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncell; c += stride) {
-    if (c == ncell) {
-      cap[c] = 0;
-      continue;
-    }
-    const int n = cnt[c];
-    // multiples of 8 slots: every bin starts on a 32-byte sector
-    cap[c] = ((long long)n + max(smin, (int)ceilf(frac * (float)n)) + 7) & ~7LL;
-  }
-}
-
-// sorted position r -> slot start[key] + (r - first[key]); first = exclusive
-// scan of the counts
-__global__ void bin_scatter(const unsigned* __restrict__ skeys,
-                            const unsigned* __restrict__ sidx, long long n,
-                            const long long* __restrict__ start,
-                            const long long* __restrict__ first, const float* const* src,
-                            const long long* __restrict__ sid, float4* __restrict__ drec,
-                            long long* __restrict__ did) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
-    const unsigned k = skeys[r], j = sidx[r];
-    const long long d = start[k] + (r - first[k]);
-    drec[2 * d] = make_float4(src[0][j], src[1][j], src[2][j], src[3][j]);
-    drec[2 * d + 1] = make_float4(src[4][j], src[5][j], src[6][j], 0.f);
-    did[d] = sid[j];
-  }
-}
-
-// export: bin c's live particles to flat[off[c] ...]
-__global__ void bin_export(const __grid_constant__ Bins b, const long long* __restrict__ off,
-                           float* const* dst, long long* __restrict__ did) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long c = gw; c < b.ncell; c += nw) {
-    const long long s0 = b.start[c];
-    const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
-    const long long o = off[c];
-    for (int r = lane; r < n; r += 32) {
-      const float4 x = b.rec[2 * (s0 + r)], y = b.rec[2 * (s0 + r) + 1];
-      dst[0][o + r] = x.x; dst[1][o + r] = x.y; dst[2][o + r] = x.z; dst[3][o + r] = x.w;
-      dst[4][o + r] = y.x; dst[5][o + r] = y.y; dst[6][o + r] = y.z;
-      did[o + r] = b.id[s0 + r];
-    }
-  }
-}
-
-// the overflow list appended after the bins' particles
-__global__ void list_export(const __grid_constant__ Bins b, long long o0, float* const* dst,
-                            long long* __restrict__ did) {
-  const long long n = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const Leaver L = b.ov[i];
-    const long long d = o0 + i;
-    dst[0][d] = L.a.x; dst[1][d] = L.a.y; dst[2][d] = L.a.z; dst[3][d] = L.a.w;
-    dst[4][d] = L.b.x; dst[5][d] = L.b.y; dst[6][d] = L.b.z;
-    did[d] = L.id;
-  }
-}
-
-__global__ void clamp_counts(int* cnt, const long long* start, int ncell) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += stride) {
-    const long long cap = start[c + 1] - start[c];
-    if (cnt[c] > cap) cnt[c] = (int)cap;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Re-slack (the cheap rebuild after an overflow): new capacities from the
-// live counts plus the overflow list's arrivals, then every bin is copied to
-// its new place and the overflow list appended (no sort: the bins are
-// already in cell order).
-__global__ void reslack_counts(const __grid_constant__ Bins b, int* __restrict__ ncount) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < b.ncell; c += stride)
-    ncount[c] = (int)min((long long)b.count[c], b.start[c + 1] - b.start[c]);
-}
-__global__ void reslack_hist(const __grid_constant__ Bins b, int* __restrict__ ncount) {
-  const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < no; i += stride) {
-    const int dest = __float_as_int(b.ov[i].b.w);
-    if (dest >= 0 && dest < b.ncell) atomicAdd(ncount + dest, 1);
-  }
-}
-// warp per bin: live particles to the new layout; ncount = live count
-__global__ void reslack_copy(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
-                             int* __restrict__ ncount, float4* __restrict__ drec,
-                             long long* __restrict__ did) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long c = gw; c < b.ncell; c += nw) {
-    const long long s0 = b.start[c];
-    const int n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
-    const long long d0 = nstart[c];
-    for (int r = lane; r < n; r += 32) {
-#pragma unroll
-      __stcs(drec + 2 * (d0 + r), __ldcs(b.rec + 2 * (s0 + r)));
-      __stcs(drec + 2 * (d0 + r) + 1, __ldcs(b.rec + 2 * (s0 + r) + 1));
-      __stcs(did + d0 + r, __ldcs(b.id + s0 + r));
-    }
-    if (lane == 0) ncount[c] = n;
-  }
-}
-__global__ void reslack_place(const __grid_constant__ Bins b, const long long* __restrict__ nstart,
-                              int* __restrict__ ncount, float4* __restrict__ drec,
-                              long long* __restrict__ did) {
-  const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < no; i += stride) {
-    const Leaver L = b.ov[i];
-    const int dest = __float_as_int(L.b.w);
-    if (dest < 0 || dest >= b.ncell) continue;
-    const long long d = nstart[dest] + atomicAdd(ncount + dest, 1);
-    drec[2 * d] = L.a;
-    drec[2 * d + 1] = make_float4(L.b.x, L.b.y, L.b.z, 0.f);
-    did[d] = L.id;
-  }
-}
-
 }  // namespace bins
 
 namespace {
@@ -1082,6 +869,7 @@ int launch_mover_bins_any(const bins::P& a, const bins::Bins& b, const int64_t* 
 // (+ the overflow and late lists).  The stat words are zeroed here; the host
 // reads them after the cycle (overflow / misplaced -> rebuild, lost -> error).
 int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
+  if (c.pbytes == 8) return bins_cycle64(c, ba, s);
   bins::P a;
   fill_params<float>(c, a);
   a.rec = c.records;
@@ -1103,7 +891,7 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   cudaMemsetAsync(b.stat, 0, bins::ST_N * sizeof(unsigned long long), s);
   int rc = launch_mover_bins_any(a, b, c.geo_i, s);
   if (rc) return rc;
-  bins::migrate_bins<<<nsm() * 8, 256, 0, s>>>(b);
+  bins::migrate_bins<float><<<nsm() * 8, 256, 0, s>>>(b);
   note_launch();
   if ((rc = bcheck("migrate_bins launch"))) return rc;
   const size_t smem = (size_t)(BP_DEP_TPB / 32) * bins::kWarpSm * sizeof(float);
@@ -1125,13 +913,46 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   return bcheck("deposit_list launch");
 }
 
+namespace {
+
+// the fast arithmetic's cell keys (fill_params / make_params: 1/d and o/d of
+// the field-precision spacing, rounded to S)
+template <typename S>
+bins::KeyGeo<S> key_geo(const Call& c) {
+  bins::KeyGeo<S> g;
+  for (int k = 0; k < 3; ++k) {
+    const double gd = c.fbytes == 8 ? c.geo_g[k] : (double)(float)c.geo_g[k];
+    const double go = c.fbytes == 8 ? c.geo_g[3 + k] : (double)(float)c.geo_g[3 + k];
+    g.idx[k] = (S)(1.0 / gd);
+    g.ogs[k] = (S)(go / gd);
+  }
+  g.nx = (int)c.geo_i[0];
+  g.ny = (int)c.geo_i[1];
+  g.nz = (int)c.geo_i[2];
+  return g;
+}
+
+template <typename S>
+bins::BinsT<S> bins_of(const BinsArgs& ba, const void* src_rec) {
+  bins::BinsT<S> b{};
+  b.rec = (typename bins::V4<S>::type*)const_cast<void*>(src_rec);
+  b.id = (long long*)ba.ids;
+  b.start = (const long long*)ba.start;
+  b.count = ba.count;
+  b.ncell = (int)ba.ncell;
+  b.ov = (bins::LeaverT<S>*)ba.overflow;
+  b.ov_cap = ba.overflow_cap;
+  b.stat = (unsigned long long*)ba.stat;
+  return b;
+}
+
 // Build step 1: cell histogram and bin layout (start = exclusive scan of the
 // capacities); returns the total slot count through *total (synchronises).
-int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin,
-              int64_t* total, cudaStream_t s) {
-  bins::P a;
-  fill_params<float>(c, a);
-  const int ncell = a.nx * a.ny * a.nz;
+template <typename S>
+int plan_t(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
+           cudaStream_t s) {
+  const bins::KeyGeo<S> g = key_geo<S>(c);
+  const int ncell = g.nx * g.ny * g.nz;
   const long long n = c.count;
   cudaMemsetAsync(count, 0, (size_t)ncell * sizeof(int), s);
   size_t tmp_bytes = 0;
@@ -1148,10 +969,10 @@ int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin,
   }
   cudaMemsetAsync(bad, 0, 16, s);
   if (n > 0) {
-    bins::bin_keys<<<nsm() * 8, 256, 0, s>>>(a, (const float*)c.x + c.start,
-                                             (const float*)c.y + c.start,
-                                             (const float*)c.z + c.start, n, nullptr, nullptr,
-                                             count, bad);
+    bins::bin_keys<S><<<nsm() * 8, 256, 0, s>>>(g, (const S*)c.x + c.start,
+                                                (const S*)c.y + c.start,
+                                                (const S*)c.z + c.start, n, nullptr, nullptr,
+                                                count, bad);
     note_launch();
   }
   bins::bin_caps<<<nsm() * 4, 256, 0, s>>>(count, ncell, (float)frac, smin, caps);
@@ -1170,11 +991,11 @@ int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin,
 }
 
 // Build step 2: stable scatter of the flat span into the planned bins.
-int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
-              int64_t* dst_ids, cudaStream_t s) {
-  bins::P a;
-  fill_params<float>(c, a);
-  const int ncell = a.nx * a.ny * a.nz;
+template <typename S>
+int fill_t(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
+           int64_t* dst_ids, cudaStream_t s) {
+  const bins::KeyGeo<S> g = key_geo<S>(c);
+  const int ncell = g.nx * g.ny * g.nz;
   const long long n = c.count;
   if (n <= 0) return 0;
   if (n > 0xffffffffLL) {
@@ -1210,23 +1031,23 @@ int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void*
   void** ptrs = (void**)p;
   cudaMemsetAsync(hist, 0, (size_t)ncell * 4, s);
   cudaMemsetAsync(bad, 0, 16, s);
-  bins::bin_keys<<<nsm() * 8, 256, 0, s>>>(a, (const float*)c.x + c.start,
-                                           (const float*)c.y + c.start,
-                                           (const float*)c.z + c.start, n, k_in, i_in, hist, bad);
+  bins::bin_keys<S><<<nsm() * 8, 256, 0, s>>>(g, (const S*)c.x + c.start,
+                                              (const S*)c.y + c.start, (const S*)c.z + c.start,
+                                              n, k_in, i_in, hist, bad);
   note_launch();
   cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, k_in, k_out, i_in, i_out, n, 0, end_bit,
                                   s);
   cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, hist, first, ncell, s);
-  const void* hp[16] = {(const float*)c.x + c.start, (const float*)c.y + c.start,
-                        (const float*)c.z + c.start, (const float*)c.u + c.start,
-                        (const float*)c.v + c.start, (const float*)c.w + c.start,
-                        (const float*)c.q + c.start, nullptr, nullptr, nullptr, nullptr,
+  const void* hp[16] = {(const S*)c.x + c.start, (const S*)c.y + c.start,
+                        (const S*)c.z + c.start, (const S*)c.u + c.start,
+                        (const S*)c.v + c.start, (const S*)c.w + c.start,
+                        (const S*)c.q + c.start, nullptr, nullptr, nullptr, nullptr,
                         nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaMemcpyAsync(ptrs, hp, sizeof(hp), cudaMemcpyHostToDevice, s);
-  bins::bin_scatter<<<nsm() * 8, 256, 0, s>>>(k_out, i_out, n, (const long long*)start, first,
-                                              (const float* const*)ptrs,
-                                              (const long long*)src_ids + c.start,
-                                              (float4*)dst_rec, (long long*)dst_ids);
+  bins::bin_scatter<S><<<nsm() * 8, 256, 0, s>>>(
+      k_out, i_out, n, (const long long*)start, first, (const S* const*)ptrs,
+      (const long long*)src_ids + c.start, (typename bins::V4<S>::type*)dst_rec,
+      (long long*)dst_ids);
   note_launch();
   cudaFreeAsync(ws, s);
   int rc = bcheck("bins_fill");
@@ -1238,17 +1059,10 @@ int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void*
 // Live-particle offsets of the bins (exclusive scan of the clamped counts)
 // and the flat copy; the overflow list follows at the end.  Returns the
 // particle total through *total (synchronises).
-int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void* const* dst,
-                int64_t* dst_ids, int64_t* total, cudaStream_t s) {
-  bins::Bins b{};
-  b.rec = (float4*)const_cast<void*>(src_rec);
-  b.id = (long long*)ba.ids;
-  b.start = (const long long*)ba.start;
-  b.count = ba.count;
-  b.ncell = (int)ba.ncell;
-  b.ov = (bins::Leaver*)ba.overflow;
-  b.ov_cap = ba.overflow_cap;
-  b.stat = (unsigned long long*)ba.stat;
+template <typename S>
+int export_t(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void* const* dst,
+             int64_t* dst_ids, int64_t* total, cudaStream_t s) {
+  const bins::BinsT<S> b = bins_of<S>(ba, src_rec);
   const int ncell = b.ncell;
   bins::clamp_counts<<<nsm() * 4, 256, 0, s>>>(ba.count, b.start, ncell);
   note_launch();
@@ -1281,11 +1095,11 @@ int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void*
   void** ptrs = nullptr;
   cudaMallocAsync(&ptrs, 8 * sizeof(void*), s);
   cudaMemcpyAsync(ptrs, dst, 7 * sizeof(void*), cudaMemcpyHostToDevice, s);
-  bins::bin_export<<<nsm() * 8, 256, 0, s>>>(b, (const long long*)offsets, (float* const*)ptrs,
-                                             (long long*)dst_ids);
+  bins::bin_export<S><<<nsm() * 8, 256, 0, s>>>(b, (const long long*)offsets, (S* const*)ptrs,
+                                                (long long*)dst_ids);
   note_launch();
   if (nov > 0) {
-    bins::list_export<<<nsm(), 256, 0, s>>>(b, nb, (float* const*)ptrs, (long long*)dst_ids);
+    bins::list_export<S><<<nsm(), 256, 0, s>>>(b, nb, (S* const*)ptrs, (long long*)dst_ids);
     note_launch();
   }
   cudaFreeAsync(tmp, s);
@@ -1296,34 +1110,14 @@ int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void*
   return rc;
 }
 
-}  // namespace bp
-
-namespace bp {
-
-namespace {
-bins::Bins bins_of(const BinsArgs& ba, const void* src_rec) {
-  bins::Bins b{};
-  b.rec = (float4*)const_cast<void*>(src_rec);
-  b.id = (long long*)ba.ids;
-  b.start = (const long long*)ba.start;
-  b.count = ba.count;
-  b.ncell = (int)ba.ncell;
-  b.ov = (bins::Leaver*)ba.overflow;
-  b.ov_cap = ba.overflow_cap;
-  b.stat = (unsigned long long*)ba.stat;
-  return b;
-}
-}  // namespace
-
-// Re-slack plan: ncount = live + overflow arrivals per bin, nstart = exclusive
-// scan of the padded capacities; *total = nstart[ncell] (synchronises).
-int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
-                      double frac, int smin, int64_t* total, cudaStream_t s) {
-  const bins::Bins b = bins_of(ba, src_rec);
+template <typename S>
+int reslack_plan_t(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
+                   double frac, int smin, int64_t* total, cudaStream_t s) {
+  const bins::BinsT<S> b = bins_of<S>(ba, src_rec);
   const int ncell = b.ncell;
-  bins::reslack_counts<<<nsm() * 4, 256, 0, s>>>(b, ncount);
+  bins::reslack_counts<S><<<nsm() * 4, 256, 0, s>>>(b, ncount);
   note_launch();
-  bins::reslack_hist<<<nsm() * 2, 256, 0, s>>>(b, ncount);
+  bins::reslack_hist<S><<<nsm() * 2, 256, 0, s>>>(b, ncount);
   note_launch();
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (long long*)nullptr, (long long*)nullptr,
@@ -1346,20 +1140,62 @@ int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int6
   return rc;
 }
 
-// Re-slack copy into dst (nstart from the plan); ncount ends as the new
-// live counts (synchronises).
-int bins_reslack_copy(const BinsArgs& ba, const void* src_rec, const int64_t* nstart,
-                      int* ncount, void* dst_rec, int64_t* dst_ids, cudaStream_t s) {
-  const bins::Bins b = bins_of(ba, src_rec);
-  bins::reslack_copy<<<nsm() * 8, 256, 0, s>>>(b, (const long long*)nstart, ncount,
-                                               (float4*)dst_rec, (long long*)dst_ids);
+template <typename S>
+int reslack_copy_t(const BinsArgs& ba, const void* src_rec, const int64_t* nstart, int* ncount,
+                   void* dst_rec, int64_t* dst_ids, cudaStream_t s) {
+  typedef typename bins::V4<S>::type V;
+  const bins::BinsT<S> b = bins_of<S>(ba, src_rec);
+  bins::reslack_copy<S><<<nsm() * 8, 256, 0, s>>>(b, (const long long*)nstart, ncount,
+                                                  (V*)dst_rec, (long long*)dst_ids);
   note_launch();
-  bins::reslack_place<<<nsm() * 2, 256, 0, s>>>(b, (const long long*)nstart, ncount,
-                                                (float4*)dst_rec, (long long*)dst_ids);
+  bins::reslack_place<S><<<nsm() * 2, 256, 0, s>>>(b, (const long long*)nstart, ncount,
+                                                   (V*)dst_rec, (long long*)dst_ids);
   note_launch();
   int rc = bcheck("bins_reslack_copy");
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = bcheck("bins_reslack_copy sync");
   return rc;
+}
+
+}  // namespace
+
+int bins_leaver_bytes(int pbytes) {
+  return pbytes == 8 ? (int)sizeof(bins::LeaverT<double>) : (int)sizeof(bins::LeaverT<float>);
+}
+
+int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
+              cudaStream_t s) {
+  return c.pbytes == 8 ? plan_t<double>(c, count, start, frac, smin, total, s)
+                       : plan_t<float>(c, count, start, frac, smin, total, s);
+}
+
+int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
+              int64_t* dst_ids, cudaStream_t s) {
+  return c.pbytes == 8 ? fill_t<double>(c, src_ids, start, dst_rec, dst_ids, s)
+                       : fill_t<float>(c, src_ids, start, dst_rec, dst_ids, s);
+}
+
+int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void* const* dst,
+                int64_t* dst_ids, int64_t* total, cudaStream_t s) {
+  return ba.pbytes == 8 ? export_t<double>(ba, src_rec, offsets, dst, dst_ids, total, s)
+                        : export_t<float>(ba, src_rec, offsets, dst, dst_ids, total, s);
+}
+
+// Re-slack plan: ncount = live + overflow arrivals per bin, nstart = exclusive
+// scan of the padded capacities; *total = nstart[ncell] (synchronises).
+int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
+                      double frac, int smin, int64_t* total, cudaStream_t s) {
+  return ba.pbytes == 8
+             ? reslack_plan_t<double>(ba, src_rec, ncount, nstart, frac, smin, total, s)
+             : reslack_plan_t<float>(ba, src_rec, ncount, nstart, frac, smin, total, s);
+}
+
+// Re-slack copy into dst (nstart from the plan); ncount ends as the new
+// live counts (synchronises).
+int bins_reslack_copy(const BinsArgs& ba, const void* src_rec, const int64_t* nstart,
+                      int* ncount, void* dst_rec, int64_t* dst_ids, cudaStream_t s) {
+  return ba.pbytes == 8
+             ? reslack_copy_t<double>(ba, src_rec, nstart, ncount, dst_rec, dst_ids, s)
+             : reslack_copy_t<float>(ba, src_rec, nstart, ncount, dst_rec, dst_ids, s);
 }
 
 }  // namespace bp

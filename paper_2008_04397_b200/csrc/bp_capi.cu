@@ -655,13 +655,15 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// Cell-binned f32 fast path (bp_bins.cu)
+// Cell-binned fast path (bp_bins.cu f32, bp_bins64.cu f64)
 namespace {
-int bins_call(Call& c, int fbytes, const void* xs, const void* ys, const void* zs,
+int bins_call(Call& c, int pbytes, int fbytes, const void* xs, const void* ys, const void* zs,
               const void* us, const void* vs, const void* ws, const void* qs, int64_t start,
               int64_t count, const double* geo_f, const double* geo_g, const int64_t* geo_i) {
-  if (fbytes != 4 && fbytes != 8) {
-    set_error("unsupported field dtype (%d bytes)", fbytes);
+  // f32 particles with f32 or f64 fields; f64 particles with f64 fields
+  if (!((pbytes == 4 && (fbytes == 4 || fbytes == 8)) || (pbytes == 8 && fbytes == 8))) {
+    set_error("unsupported dtype pair for the binned layout (particles %d, fields %d bytes)",
+              pbytes, fbytes);
     return BP_EINVAL;
   }
   int rc = check_geo(geo_g, geo_i);
@@ -671,7 +673,7 @@ int bins_call(Call& c, int fbytes, const void* xs, const void* ys, const void* z
     return BP_EINVAL;
   }
   c.op = OP_FUSED;
-  c.pbytes = 4; c.fbytes = fbytes;
+  c.pbytes = pbytes; c.fbytes = fbytes;
   c.x = const_cast<void*>(xs); c.y = const_cast<void*>(ys); c.z = const_cast<void*>(zs);
   c.u = const_cast<void*>(us); c.v = const_cast<void*>(vs); c.w = const_cast<void*>(ws);
   c.q = qs;
@@ -682,14 +684,50 @@ int bins_call(Call& c, int fbytes, const void* xs, const void* ys, const void* z
 }
 }  // namespace
 
-int bp_bins_leaver_bytes(void) { return bp::kBinsLeaverBytes; }
+int bp_bins_leaver_bytes(int pbytes) {
+  if (pbytes != 4 && pbytes != 8) {
+    set_error("particle dtype must be 4 or 8 bytes");
+    return BP_EINVAL;
+  }
+  return bp::bins_leaver_bytes(pbytes);
+}
 
-int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,
+int64_t bp_node_records_bytes(int pbytes, const int64_t* geo_i) {
+  if (pbytes != 4 && pbytes != 8) {
+    set_error("particle dtype must be 4 or 8 bytes");
+    return BP_EINVAL;
+  }
+  if (!geo_i || geo_i[0] < 1 || geo_i[1] < 1 || geo_i[2] < 1) {
+    set_error("cell counts must be >= 1");
+    return BP_EINVAL;
+  }
+  return (int64_t)bp::node_records_bytes(pbytes, geo_i);
+}
+
+int bp_node_records_build(int pbytes, int fbytes, const void* E, const void* B,
+                          const void* invvol, const int64_t* geo_i, void* records,
+                          void* stream) {
+  if (!((pbytes == 8 && fbytes == 8) || (pbytes == 4 && (fbytes == 4 || fbytes == 8)))) {
+    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
+    return BP_EINVAL;
+  }
+  if (!E || !B || !invvol || !records || !geo_i || geo_i[0] < 1 || geo_i[1] < 1 ||
+      geo_i[2] < 1 || ((uintptr_t)records % 32) != 0) {
+    set_error("node_records_build: E, B, invvol, geo_i and 32-byte aligned records required");
+    return BP_EINVAL;
+  }
+  return bp::node_records_build(pbytes, fbytes, E, B, invvol, geo_i, records,
+                                (cudaStream_t)stream)
+             ? BP_ECUDA
+             : BP_OK;
+}
+
+int bp_bins_plan(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
                  double slack_frac, int slack_min, int32_t* count, int64_t* start,
                  int64_t* total, void* stream) {
   Call c{};
-  int rc = bins_call(c, fbytes, xs, ys, zs, nullptr, nullptr, nullptr, nullptr, 0, n, geo_f,
+  int rc = bins_call(c, pbytes, fbytes, xs, ys, zs, nullptr, nullptr, nullptr, nullptr, 0, n, geo_f,
                      geo_g, geo_i);
   if (rc) return rc;
   if (!count || !start || !total || n < 0 || slack_frac < 0 || slack_min < 0) {
@@ -699,12 +737,12 @@ int bp_bins_plan(int fbytes, const void* xs, const void* ys, const void* zs, int
   return bins_plan(c, count, start, slack_frac, slack_min, total, (cudaStream_t)stream);
 }
 
-int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
+int bp_bins_fill(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs, const void* us,
                  const void* vs, const void* ws, const void* qs, const int64_t* ids, int64_t n,
                  const double* geo_f, const double* geo_g, const int64_t* geo_i,
                  const int64_t* start, void* dst_rec, int64_t* dst_ids, void* stream) {
   Call c{};
-  int rc = bins_call(c, fbytes, xs, ys, zs, us, vs, ws, qs, 0, n, geo_f, geo_g, geo_i);
+  int rc = bins_call(c, pbytes, fbytes, xs, ys, zs, us, vs, ws, qs, 0, n, geo_f, geo_g, geo_i);
   if (rc) return rc;
   if (!ids || !start || !dst_rec || ((uintptr_t)dst_rec % 16) != 0 || !dst_ids || !us || !vs ||
       !ws || !qs) {
@@ -714,7 +752,7 @@ int bp_bins_fill(int fbytes, const void* xs, const void* ys, const void* zs, con
   return bins_fill(c, ids, start, dst_rec, dst_ids, (cudaStream_t)stream);
 }
 
-int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_cycle(int pbytes, int fbytes, void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                   int64_t ncell,
                   void* leavers, int64_t leaver_cap, void* overflow, int64_t overflow_cap,
                   void* late, int64_t late_cap, uint64_t* stat, const void* records,
@@ -723,15 +761,18 @@ int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int
                   double dth, double qdt2m, double beta, double one, int n_iters, double scale,
                   int* d_status, void* stream) {
   Call c{};
-  int rc = bins_call(c, fbytes, rec, rec, rec, rec, rec, rec, rec, 0, 0, geo_f, geo_g, geo_i);
+  int rc = bins_call(c, pbytes, fbytes, rec, rec, rec, rec, rec, rec, rec, 0, 0, geo_f, geo_g,
+                     geo_i);
   if (rc) return rc;
-  if (!rec || ((uintptr_t)rec % 16) != 0 || !records || ((uintptr_t)records % 32) != 0 ||
+  // 256-bit record accesses: 32-byte aligned slots
+  if (!rec || ((uintptr_t)rec % 32) != 0 || !records || ((uintptr_t)records % 32) != 0 ||
       !acc || !invvol || !ids || !start ||
       !count || !stat || !leavers || !overflow || !late || leaver_cap < 0 ||
       leaver_cap > 0x7fffffffLL ||
       overflow_cap < 0 || late_cap < 0 ||
       n_iters < 0 || !d_status) {
-    set_error("bins_cycle: bad arguments (records 32-byte aligned, buffers, d_status required)");
+    set_error("bins_cycle: bad arguments (rec and records 32-byte aligned, buffers, d_status "
+              "required)");
     return BP_EINVAL;
   }
   if (ncell != geo_i[0] * geo_i[1] * geo_i[2]) {
@@ -740,34 +781,35 @@ int bp_bins_cycle(int fbytes, void* rec, int64_t* ids, const int64_t* start, int
   }
   c.acc = acc; c.invvol = invvol;
   c.dt = dt; c.dth = dth; c.qdt2m = qdt2m; c.beta = beta; c.one = one; c.scale = scale;
-  c.n_iters = n_iters; c.mixed = fbytes == 8; c.apply_bc = 1;
+  c.n_iters = n_iters; c.mixed = pbytes != fbytes; c.apply_bc = 1;
   c.records = records;
   c.status = d_status;
   BinsArgs ba{rec,     ids,      start,        count, ncell, leavers,
-              leaver_cap, overflow, overflow_cap, stat,  late,  late_cap};
+              leaver_cap, overflow, overflow_cap, stat,  late,  late_cap, pbytes};
   return bins_cycle(c, ba, (cudaStream_t)stream);
 }
 
-int bp_bins_export(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_export(int pbytes, const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream) {
-  if (!rec || ((uintptr_t)rec % 16) != 0 || !ids || !start || !count || !offsets || !total ||
-      ncell <= 0) {
+  if ((pbytes != 4 && pbytes != 8) || !rec || ((uintptr_t)rec % 16) != 0 || !ids || !start ||
+      !count || !offsets || !total || ncell <= 0) {
     set_error("bins_export: bad arguments");
     return BP_EINVAL;
   }
   ensure_pool();
   BinsArgs ba{nullptr, ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
-              overflow ? overflow_cap : 0, stat, nullptr, 0};
+              overflow ? overflow_cap : 0, stat, nullptr, 0, pbytes};
   return bins_export(ba, rec, offsets, dst, dst_ids, total, (cudaStream_t)stream);
 }
 
-int bp_bins_reslack(const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
+int bp_bins_reslack(int pbytes, const void* rec, int64_t* ids, const int64_t* start, int32_t* count,
                     int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                     double slack_frac, int slack_min, int32_t* new_count, int64_t* new_start,
                     void* dst_rec, int64_t* dst_ids, int64_t* total, void* stream) {
-  if (!rec || ((uintptr_t)rec % 16) != 0 || !ids || !start || !count || !new_count ||
+  if ((pbytes != 4 && pbytes != 8) || !rec || ((uintptr_t)rec % 16) != 0 || !ids || !start ||
+      !count || !new_count ||
       !new_start || !total || ncell <= 0 || slack_frac < 0 || slack_min < 0 ||
       (overflow && !stat)) {
     set_error("bins_reslack: bad arguments");
@@ -775,7 +817,7 @@ int bp_bins_reslack(const void* rec, int64_t* ids, const int64_t* start, int32_t
   }
   ensure_pool();
   BinsArgs ba{nullptr, ids,  start, count, ncell, nullptr, 0, const_cast<void*>(overflow),
-              overflow ? overflow_cap : 0, stat, nullptr, 0};
+              overflow ? overflow_cap : 0, stat, nullptr, 0, pbytes};
   if (!dst_rec)
     return bins_reslack_plan(ba, rec, new_count, new_start, slack_frac, slack_min,
                              total, (cudaStream_t)stream);

@@ -46,7 +46,7 @@ int split_fused(const Call& c, const void* rec, cudaStream_t s);
 
 // Cell-binned f32 fast path (bp_bins.cu): the bin layout of one species
 struct BinsArgs {
-  void* rec;             // 32-byte particle records x y z u | v w q 0 per slot
+  void* rec;             // particle records x y z u | v w q 0 per slot (2 x 4 scalars)
   int64_t* ids;
   const int64_t* start;  // [ncell + 1] slot offsets
   int* count;            // [ncell] live particles per bin
@@ -58,9 +58,16 @@ struct BinsArgs {
   uint64_t* stat;        // [8] counters (bp_b200.h BP_BINS_STAT_*)
   void* late;            // misplaced particles met by the deposit (same records)
   int64_t late_cap;
+  int pbytes = 4;        // particle scalar: 4 (32-byte records) or 8 (64-byte)
 };
-constexpr int kBinsLeaverBytes = 48;
+int bins_leaver_bytes(int pbytes);
 int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s);
+int bins_cycle64(const Call& c, const BinsArgs& ba, cudaStream_t s);  // bp_bins64.cu
+// node records of the generic fast arithmetic (pack_nodes: Ex Ey Ez Bx By Bz
+// invvol 0 per node, then max |invvol| in the last 32 bytes)
+size_t node_records_bytes(int pbytes, const int64_t* geo_i);
+int node_records_build(int pbytes, int fbytes, const void* E, const void* B, const void* invvol,
+                       const int64_t* geo_i, void* out, cudaStream_t s);
 int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
               cudaStream_t s);
 int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,

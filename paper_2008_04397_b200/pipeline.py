@@ -97,8 +97,8 @@ class DeviceSimulation:
     # "root": only rank 0 (where the host solve runs) gets them (reduce)
     reduce: str = "all"
     # particle layout: "flat" (the reference's SoA, sorted every sort_period
-    # cycles) or "bins" (per-cell bins kept sorted every cycle, bins.py; f32
-    # particles with the fast arithmetic); "auto" picks bins where they apply
+    # cycles) or "bins" (per-cell bins kept sorted every cycle, bins.py; the
+    # fast arithmetic, f32 or f64 particles); "auto" picks bins where they apply
     layout: str = "auto"
     # bin capacity = count + max(slack[1], slack[0] * count), rounded to 8
     # slots: a bin that fills up forces a re-slack of the species (a copy of
@@ -127,11 +127,11 @@ class DeviceSimulation:
         self._bins = [None] * len(self.species)
         self._lists = None
         self._flat_cache = None
-        binnable = self.arith == "fast" and pd == torch.float32
+        binnable = self.arith == "fast"
         if self.layout not in ("auto", "flat", "bins"):
             raise ConfigurationError(f"layout must be auto, flat or bins, not {self.layout!r}")
         if self.layout == "bins" and not binnable:
-            raise ConfigurationError("the binned layout needs f32 particles and fast arithmetic")
+            raise ConfigurationError("the binned layout needs the fast arithmetic")
         self.binned = self.layout == "bins" or (self.layout == "auto" and binnable)
         self.cycle = 0
         from .kernels import make_geo_arrays, kernel_scalars
@@ -144,13 +144,20 @@ class DeviceSimulation:
         self.mixed = 1 if npd != nfd else 0
         self.scale = float(nfd(MOMENT_SCALE))
         self._arith = {"parity": _lib.ARITH_PARITY, "fast": _lib.ARITH_FAST}[self.arith]
-        # f32 fast path: per-cell field records built once per field update
-        # (bp_field_records_build) and shared by every species' call
+        # f32 fast path: per-cell field records (bp_field_records_build); f64
+        # binned: node records (bp_node_records_build) — built once per field
+        # update and shared by every species' call
         self.records = None
+        self._records_kind = None
         self._records_fresh = False
+        gi = np.ascontiguousarray(self.geo_i, np.int64)
         if self.arith == "fast" and pd == torch.float32:
-            gi = np.ascontiguousarray(self.geo_i, np.int64)
             nbytes = int(_lib.load().bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data)))
+            self._records_kind = "cells"
+        elif self.binned:
+            nbytes = int(_lib.load().bp_node_records_bytes(8, ctypes.c_void_p(gi.ctypes.data)))
+            self._records_kind = "nodes"
+        if self._records_kind is not None:
             self.records = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=self.device)
         if self.reduce not in ("all", "root"):
             raise ConfigurationError(f"reduce must be 'all' or 'root', not {self.reduce!r}")
@@ -173,8 +180,10 @@ class DeviceSimulation:
         self._bins[sid] = BinnedSpecies(parts, self.geom, self.geo_f, self.geo_g, self.geo_i,
                                         self.E.element_size(), slack=self.bin_slack)
         n_max = max(b.n for b in self._bins if b is not None)
-        if self._lists is None or self._lists.leaver_cap < int(n_max * 0.25) + (1 << 20):
-            self._lists = TransitLists(self.device, n_max)
+        pb = parts.x.element_size()
+        if (self._lists is None or self._lists.pbytes != pb
+                or self._lists.leaver_cap < int(n_max * 0.25) + (1 << 20)):
+            self._lists = TransitLists(self.device, n_max, pbytes=pb)
 
     @property
     def particles(self):
@@ -233,8 +242,9 @@ class DeviceSimulation:
         self._records_fresh = False
 
     def _records_ptr(self, stream):
-        """Device address of the cell records for the current E/B (built on
-        first use after a field update), or None off the f32 fast path."""
+        """Device address of the cell (f32 fast) or node (f64 binned) records
+        for the current E/B (built on first use after a field update), or
+        None where the kernels build their own."""
         if self.records is None:
             return None
         base = self.records.data_ptr()
@@ -242,12 +252,22 @@ class DeviceSimulation:
         if not self._records_fresh:
             L = _lib.load()
             gi = np.ascontiguousarray(self.geo_i, np.int64)
-            rc = L.bp_field_records_build(4, self.E.element_size(),
-                                          ctypes.c_void_p(self.E.data_ptr()),
-                                          ctypes.c_void_p(self.B.data_ptr()),
-                                          ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
-                                          ctypes.c_void_p(stream.cuda_stream))
-            _lib.check(rc, "field_records_build")
+            if self._records_kind == "cells":
+                rc = L.bp_field_records_build(4, self.E.element_size(),
+                                              ctypes.c_void_p(self.E.data_ptr()),
+                                              ctypes.c_void_p(self.B.data_ptr()),
+                                              ctypes.c_void_p(gi.ctypes.data),
+                                              ctypes.c_void_p(ptr),
+                                              ctypes.c_void_p(stream.cuda_stream))
+                _lib.check(rc, "field_records_build")
+            else:
+                rc = L.bp_node_records_build(8, 8, ctypes.c_void_p(self.E.data_ptr()),
+                                             ctypes.c_void_p(self.B.data_ptr()),
+                                             ctypes.c_void_p(self.invvol.data_ptr()),
+                                             ctypes.c_void_p(gi.ctypes.data),
+                                             ctypes.c_void_p(ptr),
+                                             ctypes.c_void_p(stream.cuda_stream))
+                _lib.check(rc, "node_records_build")
             self._records_fresh = True
         return ptr
 

@@ -5,9 +5,11 @@ oracle.
 The binned mover uses the same cell records and the same arithmetic as the
 flat split mover, so particle states must stay BITWISE equal to the flat
 path's, cycle after cycle, whatever happens to the bins (leavers, overflowed
-bins, a full leaver list).  The moments differ only by the f32 summation
+bins, a full leaver list).  The f32 moments differ only by the f32 summation
 order of the per-bin sums: within the north star's f32 tolerance, written
-here as |bins - flat| <= 1e-5 * max|flat| per moment row."""
+here as |bins - flat| <= 1e-5 * max|flat| per moment row.  The f64 binned
+path (csrc/bp_bins64.cu) rounds every contribution onto the int64 lattice as
+the flat f64 fast path does, so its moments are bitwise too."""
 
 import os
 
@@ -46,6 +48,10 @@ def _by_id(p):
 
 
 def _assert_moments_close(a, b, tol=TOL):
+    if a[0].dtype == np.int64 and tol == 0:
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+        return
     for x, y in zip(a, b):
         for r in range(x.shape[0]):
             ref = x[r].astype(np.float64)
@@ -56,16 +62,15 @@ def _assert_moments_close(a, b, tol=TOL):
 def _assert_binned(sim):
     """Every exported particle lies in the cell of its bin: the export is in
     bin order, so the f32 cell keys must be non-decreasing."""
-    from paper_2008_04397_b200.kernels import make_geo_arrays
-    geo_f, _ = make_geo_arrays(sim.geom, np.float32)
     for p in sim.particles:
         h = p.to_host()
-        g = [np.float32(1.0 / np.float32(sim.geom.spacings[a])) for a in range(3)]
-        o = [np.float32(np.float32(sim.geom.origin[a]) / np.float32(sim.geom.spacings[a]))
-             for a in range(3)]
-        # the kernels' fmaf(x, 1/d, -o/d) in f64 then f32 rounding is the fma
+        t = h.x.dtype.type
+        g = [t(1.0 / t(sim.geom.spacings[a])) for a in range(3)]
+        o = [t(t(sim.geom.origin[a]) / t(sim.geom.spacings[a])) for a in range(3)]
+        # the kernels' fma(x, 1/d, -o/d): f64 then f32 rounding is the f32
+        # fma; for f64 a face-adjacent particle may round either way (allowed)
         gi = [np.minimum(np.trunc((getattr(h, c).astype(np.float64) * g[a] - o[a])
-                                  .astype(np.float32)).astype(np.int64), n - 1)
+                                  .astype(t)).astype(np.int64), n - 1)
               for a, (c, n) in enumerate(zip("xyz", sim.geom.counts))]
         key = gi[0] + sim.geom.nx * (gi[1] + sim.geom.ny * gi[2])
         # rounding of the emulated fma can move a particle sitting on a cell
@@ -74,8 +79,14 @@ def _assert_binned(sim):
         assert (np.diff(key) < 0).mean() < 1e-3
 
 
-def test_build_export_roundtrip(gpu):
-    geom, species, prec, bufs, fields = _gem()
+def _tol(label):
+    """moments: f32 per-bin sums within TOL, f64 bitwise"""
+    return 0 if label == "double" else TOL
+
+
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_build_export_roundtrip(gpu, label):
+    geom, species, prec, bufs, fields = _gem(label=label)
     sim = _sim(geom, species, prec, bufs, "bins")
     assert sim.binned
     for b, p in zip(bufs, sim.particles):
@@ -88,15 +99,16 @@ def test_build_export_roundtrip(gpu):
     _assert_binned(sim)
 
 
-@pytest.mark.parametrize("label", ["single", "mixed"])
+@pytest.mark.parametrize("label", ["single", "mixed", "double"])
 def test_bins_match_flat_bitwise_particles(gpu, label):
     geom, species, prec, bufs, fields = _gem(label=label)
     a = _sim(geom, species, prec, bufs, "bins")
     b = _sim(geom, species, prec, bufs, "flat")
+    assert a.binned and not b.binned
     for cyc in range(6):
         a.run_cycle(fields.E, fields.B)
         b.run_cycle(fields.E, fields.B)
-        _assert_moments_close(b.moments_host(), a.moments_host())
+        _assert_moments_close(b.moments_host(), a.moments_host(), _tol(label))
     for pa, pb in zip(a.particles, b.particles):
         da, db = _by_id(pa), _by_id(pb)
         for k in da:
@@ -107,21 +119,23 @@ def test_bins_match_flat_bitwise_particles(gpu, label):
     _assert_binned(a)
 
 
-def test_bins_overflow_and_full_leaver_list(gpu):
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_bins_overflow_and_full_leaver_list(gpu, label):
     """No slack at all (every arriving leaver overflows its bin) and a leaver
     list of a few slots (most leavers stay misplaced): rebuilds every cycle,
     the particles still bitwise the flat path's, moments within tolerance."""
     from paper_2008_04397_b200.bins import TransitLists
-    geom, species, prec, bufs, fields = _gem(seed=9)
+    geom, species, prec, bufs, fields = _gem(seed=9, label=label)
     a = _sim(geom, species, prec, bufs, "bins", bin_slack=(0.0, 0))
     b = _sim(geom, species, prec, bufs, "flat")
     for cyc in range(4):
         if cyc == 2:
-            a._lists = TransitLists(a.device, 0)   # 4096 slots: one bin claim's worth
+            # 1M slots, of which the mover may list 3
+            a._lists = TransitLists(a.device, 0, pbytes=a._lists.pbytes)
             a._lists.leaver_cap = 3
         a.run_cycle(fields.E, fields.B)
         b.run_cycle(fields.E, fields.B)
-        _assert_moments_close(b.moments_host(), a.moments_host())
+        _assert_moments_close(b.moments_host(), a.moments_host(), _tol(label))
     assert sum(b_.rebuilds for b_ in a._bins) >= 2
     for pa, pb in zip(a.particles, b.particles):
         da, db = _by_id(pa), _by_id(pb)
@@ -161,11 +175,12 @@ def test_bins_against_oracle(gpu, oracle):
         _assert_moments_close([oracle_fold], [ag], tol=1e-4)
 
 
-def test_bins_match_flat_many_per_bin(gpu):
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_bins_match_flat_many_per_bin(gpu, label):
     """Bins of several 32-particle tiles (ppc 125, as the C3 benchmark):
     four cycles bitwise against the flat path, no overflow, no misplaced."""
     geom, species, prec, bufs, fields = _gem(cells=(32, 16, 16), box=(6.4, 3.2, 3.2), ppc=125,
-                                             seed=4, e_amp=1e-4)
+                                             seed=4, e_amp=1e-4, label=label)
     a = _sim(geom, species, prec, bufs, "bins")
     b = _sim(geom, species, prec, bufs, "flat")
     for cyc in range(4):
@@ -173,21 +188,22 @@ def test_bins_match_flat_many_per_bin(gpu):
         b.run_cycle(fields.E, fields.B)
         print(cyc, a.bin_stats())
         assert all(s[1] == 0 and s[2] == 0 and s[3] == 0 for s in a.bin_stats()), a.bin_stats()
-        _assert_moments_close(b.moments_host(), a.moments_host())
+        _assert_moments_close(b.moments_host(), a.moments_host(), _tol(label))
     for pa, pb in zip(a.particles, b.particles):
         da, db = _by_id(pa), _by_id(pb)
         for k in da:
             assert np.array_equal(da[k], db[k]), k
 
 
-def test_bins_hole_cap_fallback_bitwise(gpu):
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_bins_hole_cap_fallback_bitwise(gpu, label):
     """Cells so small that most of a bin's 600 particles leave it every cycle
     (more than the mover's 256 listed leavers per bin): the excess stays
     misplaced, is deposited from the late list, and the host rebuilds the
     bins — the particles still bitwise the flat path's, moments within
     tolerance."""
     geom, species, prec, bufs, fields = _gem(cells=(4, 4, 4), box=(0.04, 0.04, 0.04), ppc=600,
-                                             seed=5, e_amp=1e-4)
+                                             seed=5, e_amp=1e-4, label=label)
     a = _sim(geom, species, prec, bufs, "bins")
     b = _sim(geom, species, prec, bufs, "flat")
     misplaced = 0
@@ -197,10 +213,49 @@ def test_bins_hole_cap_fallback_bitwise(gpu):
         misplaced += sum(s[2] for s in a.bin_stats())
         # 600 particles per cell (50x the other tests' per-node sums, in a
         # different order): the north star's 1e-4
-        _assert_moments_close(b.moments_host(), a.moments_host(), tol=1e-4)
+        _assert_moments_close(b.moments_host(), a.moments_host(),
+                              tol=0 if label == "double" else 1e-4)
     assert misplaced > 0
     assert sum(b_.rebuilds for b_ in a._bins) >= 1
     for pa, pb in zip(a.particles, b.particles):
         da, db = _by_id(pa), _by_id(pb)
         for k in da:
             assert np.array_equal(da[k], db[k]), k
+
+
+def test_bins64_against_oracle(gpu, oracle):
+    """Three cycles of the f64 binned path against the reference arithmetic
+    (CPU oracle, double): particles within the north star's 1e-10 of each
+    array's max, moments within 1e-10 of the row max + 4 quanta (a half
+    quantum rounds either way, tests/test_gpu_fullsize.py)."""
+    from paper_2008_04397_b200 import kernels as K
+    from paper_2008_04397_b200.fields import MOMENT_SCALE, fold_periodic
+    geom, species, prec, bufs, fields = _gem(cells=(32, 16, 8), box=(12.8, 6.4, 3.2), ppc=16,
+                                             label="double")
+    a = _sim(geom, species, prec, bufs, "bins")
+    assert a.binned
+    geo_f, geo_i = K.make_geo_arrays(geom, np.float64)
+    inv = geom.inv_node_volume(np.float64)
+    ref = [b.copy() for b in bufs]
+    for cyc in range(3):
+        a.run_cycle(fields.E, fields.B)
+        acc_gpu = a.moments_host()
+        for s, r, ag in zip(species, ref, acc_gpu):
+            sc = K.kernel_scalars(s, 0.25, 1.0, np.float64)
+            acc = np.zeros((10,) + geom.node_shape, np.int64)
+            st = oracle.fused_parallel(r.x, r.y, r.z, r.u, r.v, r.w, r.q_p, 0, r.n, fields.E,
+                                       fields.B, acc, inv, geo_f, geo_f, geo_i, sc["dt"],
+                                       sc["dth"], sc["qdt2m"], sc["beta"], sc["one"], 3,
+                                       np.float64(MOMENT_SCALE), 0, os.cpu_count() or 1)
+            assert st == 0
+            fold_periodic(acc, geom)
+            for m in range(10):
+                bound = 1e-10 * np.abs(acc[m]).max() + 4
+                assert np.abs(ag[m] - acc[m]).max() <= bound, (cyc, m)
+    for r, p in zip(ref, a.particles):
+        d = _by_id(p)
+        o = np.argsort(r.ids)
+        for k in "xyzuvw":
+            rk = getattr(r, k)[o]
+            err = np.abs(d[k] - rk).max() / max(np.abs(rk).max(), 1e-300)
+            assert err <= 1e-10, (k, err)
