@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-shuffled", action="store_true")
+    ap.add_argument("--no-c2-double", action="store_true",
+                    help="skip the C2 f64 leg (extra.c2_double)")
     ap.add_argument("--bin-slack", default=None,
                     help="binned layout headroom 'frac,min' (DeviceSimulation.bin_slack)")
     return ap.parse_args()
@@ -467,6 +469,12 @@ def main_ours(args):
         del psim, pt
         torch.cuda.empty_cache()
 
+    # BASELINE configs[1] (C2, 2D GEM 256 x 128 x 1, f64): the binned f64 fast
+    # path, the flat generic f64 fast path and the bitwise arithmetic, with
+    # their own clocks (one GPU; skipped when the headline already is f64)
+    if world == 1 and not args.no_c2_double and args.precision != "double":
+        extra["c2_double"] = c2_double_leg(dev)
+
     # unsorted worst case: the flat layout with every species randomly
     # permuted and no sort (each particle's cell record and deposit target is
     # a random cell: L2 instead of L1 reuse)
@@ -503,6 +511,50 @@ def main_ours(args):
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def c2_double_leg(dev, steps=10, warmup=3):
+    """C2 in double precision (BASELINE configs[1]): particles/s per step of
+    the f64 binned fast path (csrc/bp_bins64.cu), of the flat generic f64
+    fast path and of the bitwise reference arithmetic, each over `steps`
+    device-timed cycles after `warmup`, one NVML clock record for all."""
+    import torch
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import (GemInit, gem_fields, gem_geometry, gem_species,
+                                           init_gem_device, smooth_e_field)
+    from paper_2008_04397_b200.pipeline import DeviceSimulation
+    geom = gem_geometry((256, 128, 1))
+    species = gem_species(125)
+    prec = PrecisionMode.from_label("double")
+    f = gem_fields(geom, GemInit(), prec)
+    f.E[...] = smooth_e_field(geom, E_AMP, f.E.dtype)
+    n_total = geom.n_cells * 125 * len(species)
+    out = {"workload": "gem2d_256x128x1_ppc125x4", "particles": n_total, "steps": steps,
+           "warmup": warmup, "unit": UNIT}
+    with ClockMonitor(dev.index) as mon:
+        for name, arith, layout in (("bins_fast", "fast", "bins"), ("flat_fast", "fast", "flat"),
+                                    ("parity", "parity", "flat")):
+            sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=arith,
+                                   sort_period=10, device=dev, layout=layout)
+            for sid, p in enumerate(init_gem_device(geom, species, dev, precision=prec)):
+                sim.load_species(sid, p)
+            sim.set_fields(f.E, f.B)
+            sim.sort()
+            for _ in range(warmup):
+                sim.run_cycle()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                sim.run_cycle()
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = n_total * steps / (e0.elapsed_time(e1) * 1e-3)
+            del sim
+            torch.cuda.empty_cache()
+    out["bins_over_parity"] = out["bins_fast"] / out["parity"]
+    out["clocks"] = mon.summary()
+    return out
 
 
 def shuffled_leg(args, sim, geom, species, prec, fields, dist, dev, n_total):

@@ -105,7 +105,10 @@ __device__ __forceinline__ int bin_of(const SP& a, const FastScalars<double>& s,
 // listed (x..w, q, id, new cell) and leaves a hole; after the bin's last tile
 // the holes below the new count take the bin's trailing stayers.  The next
 // tile's records (or the next bin's first tile) load during the push.
-__global__ void __launch_bounds__(kTpb) mover_bins64(const __grid_constant__ SP a,
+#ifndef BP_MOV64_MINB
+#define BP_MOV64_MINB 5  // resident 128-thread blocks per SM (measured at C2: 4 -> 0.248 ms, 5 -> 0.242, 6 -> 0.256)
+#endif
+__global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(const __grid_constant__ SP a,
                                                      const __grid_constant__ Bins b) {
   __shared__ unsigned short holes_s[kWarps][kHoleCap];
   __shared__ int lvslot_s[kWarps][kHoleCap];

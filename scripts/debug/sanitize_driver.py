@@ -18,7 +18,7 @@ geom = gem_geometry((16, 8, 8), (3.2, 1.6, 1.6))
 species = gem_species(48)
 dev = torch.device("cuda", 0)
 runs = [("single", "fast", "flat"), ("single", "fast", "bins"), ("single", "parity", "flat"),
-        ("double", "fast", "flat"), ("mixed", "parity", "flat")]
+        ("double", "fast", "flat"), ("double", "fast", "bins"), ("mixed", "parity", "flat")]
 for label, arith, layout in runs:
     prec = PrecisionMode.from_label(label)
     sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith=arith, sort_period=2,

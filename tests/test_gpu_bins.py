@@ -259,3 +259,41 @@ def test_bins64_against_oracle(gpu, oracle):
             rk = getattr(r, k)[o]
             err = np.abs(d[k] - rk).max() / max(np.abs(rk).max(), 1e-300)
             assert err <= 1e-10, (k, err)
+
+
+def test_bins64_c2_fullsize_bitwise(gpu):
+    """C2 (BASELINE configs[1]: 2D GEM 256 x 128 x 1, ppc 125, four species,
+    16.4M f64 particles) on the bins, loaded by the bit-exact device loader:
+    two cycles bitwise the flat f64 fast path — every particle and the int64
+    lattice — with leavers but no overflow or misplaced particle."""
+    import torch
+    from paper_2008_04397_b200.config import PrecisionMode
+    from paper_2008_04397_b200.gem import (GemInit, gem_fields, gem_geometry, gem_species,
+                                           init_gem_device, smooth_e_field)
+    from paper_2008_04397_b200.pipeline import DeviceSimulation
+    geom = gem_geometry((256, 128, 1))
+    species = gem_species(125)
+    prec = PrecisionMode.from_label("double")
+    f = gem_fields(geom, GemInit(), prec)
+    f.E[...] = smooth_e_field(geom, 2e-3, f.E.dtype)
+    dev = torch.device("cuda", 0)
+    sims = []
+    for layout in ("bins", "flat"):
+        sim = DeviceSimulation(geom, species, dt=0.25, precision=prec, arith="fast",
+                               sort_period=10, device=dev, layout=layout)
+        for sid, p in enumerate(init_gem_device(geom, species, dev, precision=prec)):
+            sim.load_species(sid, p)
+        sim.set_fields(f.E, f.B)
+        sims.append(sim)
+    a, b = sims
+    assert a.binned and not b.binned
+    for _ in range(2):
+        a.run_cycle()
+        b.run_cycle()
+        _assert_moments_close(b.moments_host(), a.moments_host(), 0)
+    st = a.bin_stats()
+    assert all(s[0] > 0 and s[1] == 0 and s[2] == 0 and s[3] == 0 for s in st), st
+    for pa, pb in zip(a.particles, b.particles):
+        da, db = _by_id(pa), _by_id(pb)
+        for k in da:
+            assert np.array_equal(da[k], db[k]), k
