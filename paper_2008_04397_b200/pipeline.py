@@ -132,6 +132,12 @@ class DeviceSimulation:
             raise ConfigurationError(f"layout must be auto, flat or bins, not {self.layout!r}")
         if self.layout == "bins" and not binnable:
             raise ConfigurationError("the binned layout needs the fast arithmetic")
+        if self.layout == "auto" and binnable:
+            # the bins hold two buffer sets (live + the re-slack's destination)
+            # of (1 + slack) slots per particle: decks whose sets would not fit
+            # the device (f64 C5 at 1e9 particles: ~300 GB) stay flat
+            binnable = self.bins_bytes_estimate() <= 0.92 * torch.cuda.get_device_properties(
+                self.device).total_memory
         self.binned = self.layout == "bins" or (self.layout == "auto" and binnable)
         self.cycle = 0
         from .kernels import make_geo_arrays, kernel_scalars
@@ -166,6 +172,21 @@ class DeviceSimulation:
             self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
         else:
             self.rank, self.world = 0, 1
+
+    def bins_bytes_estimate(self, world=None):
+        """Device bytes of the binned layout for this deck on one rank: two
+        buffer sets of records (8 scalars) + int64 ids, count + max(min,
+        frac x count) slots per cell (bins.py), 3% headroom."""
+        if world is None:
+            world = 1
+            if self.distributed:
+                import torch.distributed as dist
+                world = dist.get_world_size(self.group)
+        frac, smin = self.bin_slack
+        nc = int(self.geom.n_cells)
+        slots = sum(nc * (sp.ppc + max(smin, frac * sp.ppc)) for sp in self.species) / world
+        pbytes = 4 if self.pdt == self.torch.float32 else 8
+        return 2 * 1.03 * slots * (8 * pbytes + 8)
 
     # ------------------------------------------------------------ loading
     def load_species(self, sid, parts):
