@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   // lv_used of them taken (starts "full": the first leaver claims a chunk)
   long long lv_base = 0, lv_next = 0;
   int lv_used = kLvChunk;
-  unsigned phase[2] = {0u, 0u};
+  // mbarrier phase parity of buffer k in bit k (a register: an array indexed
+  // by bf would live in local memory)
+  unsigned phases = 0u;
   int bf = 0;
 #if BP_MOVER_WINDOW
   int c0 = claim_win();
@@ -406,12 +408,12 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   while (c0 < b.ncell) {
     const int c1 = min(c0 + b.move_claim, b.ncell);
 #if BP_MOVER_WINDOW
-    mbar_wait(&bars[0], phase[0]);
-    phase[0] ^= 1u;
+    mbar_wait(&bars[0], phases & 1u);
+    phases ^= 1u;
 #else
     const int cn = claim(bf ^ 1);  // the next claim's records load meanwhile
-    mbar_wait(&bars[bf], phase[bf]);
-    phase[bf] ^= 1u;
+    mbar_wait(&bars[bf], (phases >> bf) & 1u);
+    phases ^= 1u << bf;
 #endif
     long long s0 = b.start[c0];
     int n = (int)min((long long)b.count[c0], b.start[c0 + 1] - s0);
