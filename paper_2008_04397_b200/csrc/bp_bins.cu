@@ -76,6 +76,13 @@ __device__ __forceinline__ void st_rec_stream(float4* p, const float4& a, const 
                "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
                : "memory");
 }
+// slot q's record (2 float4): one 32 x 32 -> 64-bit multiply-add (the f32
+// mover keeps slot indices in 32 bits; bins_plan refuses layouts of 2^31 or
+// more slots)
+__device__ __forceinline__ float4* slot_rec(float4* rec, int q) {
+  return reinterpret_cast<float4*>(reinterpret_cast<char*>(rec) + (size_t)(unsigned)q * 32u);
+}
+
 constexpr int kHoleCap = 256;    // leavers per bin per cycle tracked for the refill (more: misplaced, rebuild)
 constexpr int kMoveClaim = 8;    // bins per mover work claim (at most; Bins::move_claim)
 constexpr int kLvChunk = 128;    // leaver slots per warp reservation
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 #endif
   // the warp's current chunk of leaver slots [lv_base, lv_base + kLvChunk),
   // lv_used of them taken (starts "full": the first leaver claims a chunk)
-  long long lv_base = 0, lv_next = 0;
+  int lv_base = 0, lv_next = 0;
   int lv_used = kLvChunk;
   // mbarrier phase parity of buffer k in bit k (a register: an array indexed
   // by bf would live in local memory)
@@ -398,10 +405,10 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 #endif
   // prefetched particle (one per lane) and the slot it came from
   float4 n1a = make_float4(0.f, 0.f, 0.f, 0.f), n1b = n1a;
-  auto fetch = [&](long long q, bool ok) {
+  auto fetch = [&](int q, bool ok) {
     if (ok) {
       // streaming loads (read once per cycle): the 32-byte record
-      ld_rec_stream(b.rec + 2 * q, n1a, n1b);
+      ld_rec_stream(slot_rec(b.rec, q), n1a, n1b);
     }
   };
   float4 R[12];
@@ -415,19 +422,19 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
     mbar_wait(&bars[bf], (phases >> bf) & 1u);
     phases ^= 1u << bf;
 #endif
-    long long s0 = b.start[c0];
-    int n = (int)min((long long)b.count[c0], b.start[c0 + 1] - s0);
+    int s0 = (int)b.start[c0];
+    int n = min(b.count[c0], (int)b.start[c0 + 1] - s0);
     fetch(s0 + lane, (int)lane < n);
     bool pf_ok = true;  // (warp-uniform) n1 holds this bin's first tile
     Ijk q3 = ijk_of(a, c0);
     for (int c = c0; c < c1; ++c, q3 = ijk_advance(a, q3, 1)) {
       // metadata of the next bin of the claim (its first tile is prefetched
       // during this bin's last tile)
-      long long s1 = 0;
+      int s1 = 0;
       int n_1 = 0;
       if (c + 1 < c1) {
-        s1 = b.start[c + 1];
-        n_1 = (int)min((long long)b.count[c + 1], b.start[c + 2] - s1);
+        s1 = (int)b.start[c + 1];
+        n_1 = min(b.count[c + 1], (int)b.start[c + 2] - s1);
       }
       if (n > 0) {
         if (!pf_ok) fetch(s0 + lane, (int)lane < n);
@@ -445,7 +452,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
         for (int t0 = 0; t0 < n; t0 += 32) {
           const int r = t0 + (int)lane;
           const bool valid = r < n;
-          const long long p = s0 + r;
+          const int p = s0 + r;
           float xp = n1a.x, yp = n1a.y, zp = n1a.z, un = n1a.w, vn = n1b.x, wn = n1b.y;
           const float qp = n1b.z;
           if (t0 + 32 < n) fetch(p + 32, r + 32 < n);
@@ -489,11 +496,10 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
             unsigned long long nb = 0;
             if (lane == 0) nb = atomicAdd(&b.stat[ST_LEAVERS], (unsigned long long)kLvChunk);
             nb = __shfl_sync(0xffffffffu, nb, 0);
-            lv_next = (long long)nb;
+            lv_next = (int)min(nb, (unsigned long long)0x7fffff00);
           }
           const int room = kLvChunk - lv_used;  // slots left in the current chunk
-          const long long slot =
-              rank < room ? lv_base + lv_used + rank : lv_next + (rank - room);
+          const int slot = rank < room ? lv_base + lv_used + rank : lv_next + (rank - room);
           // accepted leavers are a prefix in rank order (hole index grows
           // with the rank), so their hole indices stay contiguous
           listed = leave && slot < b.lv_cap && nh + rank < kHoleCap && r < 65536;
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
             rec[0] = make_float4(xp, yp, zp, un);
             rec[1] = make_float4(vn, wn, qp, __int_as_float(dest));
             holes[nh + rank] = (unsigned short)r;
-            lvslot[nh + rank] = (int)slot;
+            lvslot[nh + rank] = slot;
           } else if (leave) {
             // stays here as a misplaced particle (slow paths; host rebuilds)
             atomicAdd(&b.stat[ST_MISPLACED], 1ULL);
@@ -523,7 +529,8 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
         // written; write-back stores, so the refill and the migration find
         // the bin's lines in L2
         if (valid && st == ST_OK) {
-          st_rec_stream(b.rec + 2 * p, make_float4(xp, yp, zp, un), make_float4(vn, wn, qp, 0.f));
+          st_rec_stream(slot_rec(b.rec, p), make_float4(xp, yp, zp, un),
+                        make_float4(vn, wn, qp, 0.f));
         }
       }
         __syncwarp();
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
             // this lane's leaver (k < nh) and refill pair (k < nlow)
             long long lid = 0;
             if (k < nh) lid = b.id[s0 + holes[k]];
-            long long src = 0, dst = 0;
+            int src = 0, dst = 0;
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
             long long rid = 0;
             if (k < nlow) {
@@ -555,15 +562,15 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
               }
               src = s0 + t;
               dst = s0 + holes[k];
-              ra = b.rec[2 * src];
-              rb = b.rec[2 * src + 1];
+              ra = slot_rec(b.rec, src)[0];
+              rb = slot_rec(b.rec, src)[1];
               rid = b.id[src];
             }
             if (k < nh) b.lv[lvslot[k]].id = lid;
             __syncwarp();
             if (k < nlow) {
-              b.rec[2 * dst] = ra;
-              b.rec[2 * dst + 1] = rb;
+              slot_rec(b.rec, dst)[0] = ra;
+              slot_rec(b.rec, dst)[1] = rb;
               b.id[dst] = rid;
             }
           }
@@ -1164,10 +1171,21 @@ int bins_leaver_bytes(int pbytes) {
   return pbytes == 8 ? (int)sizeof(bins::LeaverT<double>) : (int)sizeof(bins::LeaverT<float>);
 }
 
+// the f32 mover indexes slots in 32 bits
+static int check_f32_slots(int pbytes, int rc, const int64_t* total) {
+  if (!rc && pbytes == 4 && *total >= 0x7fffffffLL) {
+    set_error("binned layout of %lld slots: the f32 bins hold < 2^31 (use a smaller slack or "
+              "the flat layout)", (long long)*total);
+    return -1;
+  }
+  return rc;
+}
+
 int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
               cudaStream_t s) {
-  return c.pbytes == 8 ? plan_t<double>(c, count, start, frac, smin, total, s)
-                       : plan_t<float>(c, count, start, frac, smin, total, s);
+  const int rc = c.pbytes == 8 ? plan_t<double>(c, count, start, frac, smin, total, s)
+                               : plan_t<float>(c, count, start, frac, smin, total, s);
+  return check_f32_slots(c.pbytes, rc, total);
 }
 
 int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,
@@ -1186,9 +1204,10 @@ int bins_export(const BinsArgs& ba, const void* src_rec, int64_t* offsets, void*
 // scan of the padded capacities; *total = nstart[ncell] (synchronises).
 int bins_reslack_plan(const BinsArgs& ba, const void* src_rec, int* ncount, int64_t* nstart,
                       double frac, int smin, int64_t* total, cudaStream_t s) {
-  return ba.pbytes == 8
-             ? reslack_plan_t<double>(ba, src_rec, ncount, nstart, frac, smin, total, s)
-             : reslack_plan_t<float>(ba, src_rec, ncount, nstart, frac, smin, total, s);
+  const int rc =
+      ba.pbytes == 8 ? reslack_plan_t<double>(ba, src_rec, ncount, nstart, frac, smin, total, s)
+                     : reslack_plan_t<float>(ba, src_rec, ncount, nstart, frac, smin, total, s);
+  return check_f32_slots(ba.pbytes, rc, total);
 }
 
 // Re-slack copy into dst (nstart from the plan); ncount ends as the new

@@ -768,7 +768,7 @@ int bp_bins_cycle(int pbytes, int fbytes, void* rec, int64_t* ids, const int64_t
   if (!rec || ((uintptr_t)rec % 32) != 0 || !records || ((uintptr_t)records % 32) != 0 ||
       !acc || !invvol || !ids || !start ||
       !count || !stat || !leavers || !overflow || !late || leaver_cap < 0 ||
-      leaver_cap > 0x7fffffffLL ||
+      leaver_cap > 0x7fffff00LL ||
       overflow_cap < 0 || late_cap < 0 ||
       n_iters < 0 || !d_status) {
     set_error("bins_cycle: bad arguments (rec and records 32-byte aligned, buffers, d_status "
