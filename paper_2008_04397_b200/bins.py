@@ -27,6 +27,16 @@ from .particles import ARRAYS, DeviceParticles
 STAT_LEAVERS, STAT_OVERFLOW, STAT_MISPLACED, STAT_LOST = 0, 1, 2, 3
 
 
+def layout_bytes(n_cells, ppcs, slack, pbytes, world=1):
+    """Device bytes of the binned layout of a deck on one rank: two buffer
+    sets (live + the re-slack's destination) of records (8 scalars of
+    pbytes) + int64 ids, count + max(slack_min, slack_frac x count) slots per
+    cell and species, 3% headroom (BinnedSpecies._alloc_set)."""
+    frac, smin = slack
+    slots = sum(n_cells * (p + max(smin, frac * p)) for p in ppcs) / max(1, world)
+    return 2 * 1.03 * slots * (8 * pbytes + 8)
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 

@@ -174,19 +174,17 @@ class DeviceSimulation:
             self.rank, self.world = 0, 1
 
     def bins_bytes_estimate(self, world=None):
-        """Device bytes of the binned layout for this deck on one rank: two
-        buffer sets of records (8 scalars) + int64 ids, count + max(min,
-        frac x count) slots per cell (bins.py), 3% headroom."""
+        """Device bytes of the binned layout for this deck on one rank
+        (bins.layout_bytes)."""
         if world is None:
             world = 1
             if self.distributed:
                 import torch.distributed as dist
                 world = dist.get_world_size(self.group)
-        frac, smin = self.bin_slack
-        nc = int(self.geom.n_cells)
-        slots = sum(nc * (sp.ppc + max(smin, frac * sp.ppc)) for sp in self.species) / world
+        from .bins import layout_bytes
         pbytes = 4 if self.pdt == self.torch.float32 else 8
-        return 2 * 1.03 * slots * (8 * pbytes + 8)
+        return layout_bytes(int(self.geom.n_cells), [sp.ppc for sp in self.species],
+                            self.bin_slack, pbytes, world)
 
     # ------------------------------------------------------------ loading
     def load_species(self, sid, parts):

@@ -113,3 +113,22 @@ def test_checkpoint_v2_keeps_charge_and_ids(tmp_path):
     assert back.species_id == 2
     for nm in ("x", "y", "z", "u", "v", "w", "q_p", "ids"):
         assert np.array_equal(getattr(back, nm), getattr(buf, nm)), nm
+
+
+def test_binned_layout_estimate_and_auto_rule():
+    """bins.layout_bytes, the memory rule behind DeviceSimulation's
+    layout="auto": C3 f32 (the headline, ~43 GB) and the C5 sweep's f32 deck
+    at 1e9 particles (~103 GB) fit a 180 GB B200 with its two buffer sets,
+    C5 f64 at 1e9 (~185 GB) does not (it stays flat), and the estimate
+    splits over ranks."""
+    from paper_2008_04397_b200.bins import layout_bytes
+    dev = 0.92 * 179.5e9
+    c3 = layout_bytes(128 * 64 * 64, [125] * 4, (1.0, 64), 4)
+    assert 40e9 < c3 < 46e9 and c3 < dev
+    ppc = round(1e9 / (128 * 64 * 64))
+    c5_f32 = layout_bytes(128 * 64 * 64, [ppc], (0.25, 16), 4)
+    c5_f64 = layout_bytes(128 * 64 * 64, [ppc], (0.25, 16), 8)
+    assert c5_f32 < dev < c5_f64
+    assert abs(layout_bytes(128 * 64 * 64, [ppc], (0.25, 16), 8, world=8) - c5_f64 / 8) < 1.0
+    # a slack minimum dominates sparse cells: ppc 12 with min 64 -> 76 slots
+    assert layout_bytes(10, [12], (1.0, 64), 4) == 2 * 1.03 * 10 * 76 * 40
