@@ -228,11 +228,10 @@ int bp_fold_periodic_i64(int64_t* acc, int64_t rows, const int64_t* geo_i, void*
  *                of the call, the overflow list feeds the rebuild, the late
  *                list holds misplaced particles met by the deposit; it may alias the
  *                leaver list, which the migration has drained by then), with
- *                `records` = for f32 particles the per-cell records of
- *                bp_field_records_build (pbytes 4), for f64 particles the
- *                node records of bp_node_records_build (pbytes 8) — the f64
- *                cycle is bitwise the flat f64 fast path's (particles and
- *                lattice); asynchronous; the worst
+ *                `records` = the per-cell records of bp_field_records_build
+ *                in the particle precision (pbytes) — the f64 cycle is
+ *                bitwise the flat f64 fast path's (particles and lattice);
+ *                asynchronous; the worst
  *                particle status goes to *d_status (atomicMax).  stat[8]
  *                (uint64) counts leavers (0), overflowed leavers (1),
  *                misplaced particles (2) and lost particles (3): after the
@@ -280,15 +279,6 @@ int bp_bins_export(int pbytes, const void* rec, int64_t* ids, const int64_t* sta
                    int64_t ncell, const void* overflow, int64_t overflow_cap, uint64_t* stat,
                    int64_t* offsets, void* const* dst, int64_t* dst_ids, int64_t* total,
                    void* stream);
-
-/* Node records of the generic fast arithmetic (f64 binned cycle): Ex Ey Ez
- * Bx By Bz invvol 0 per node in the particle precision (pbytes), then max
- * |invvol| (f64) in the last 32 bytes; bp_node_records_bytes() gives the
- * size of the (32-byte aligned) device buffer.  Asynchronous. */
-int64_t bp_node_records_bytes(int pbytes, const int64_t* geo_i);
-int bp_node_records_build(int pbytes, int fbytes, const void* E, const void* B,
-                          const void* invvol, const int64_t* geo_i, void* records,
-                          void* stream);
 
 /* ------------------------------------------------------------------------
  * Bit-exact device loader: one species of the reference's init_maxwellian

@@ -31,7 +31,7 @@ EXPORTS = (
     "bp_field_records_bytes", "bp_field_records_build", "bp_fused_span_rec",
     "bp_timing_enable", "bp_timing_read",
     "bp_bins_leaver_bytes", "bp_bins_plan", "bp_bins_fill", "bp_bins_cycle", "bp_bins_export",
-    "bp_bins_reslack", "bp_node_records_bytes", "bp_node_records_build", "bp_init_maxwellian",
+    "bp_bins_reslack", "bp_init_maxwellian",
 )
 
 _P = ctypes.c_void_p
@@ -71,8 +71,6 @@ _SIGS = {
     "bp_moments_total": (_INT, [_P, _INT, _I64, _P, _P]),
     "bp_susceptibility": (_INT, [_P, _P, _INT, _INT, _D, _D, _I64, _P, _P]),
     "bp_bins_leaver_bytes": (_INT, [_INT]),
-    "bp_node_records_bytes": (_I64, [_INT, _P]),
-    "bp_node_records_build": (_INT, [_INT, _INT, _P, _P, _P, _P, _P, _P]),
     "bp_bins_plan": (_INT, [_INT, _INT, _P, _P, _P, _I64, _P, _P, _P, _D, _INT, _P, _P, _P, _P]),
     "bp_bins_fill": (_INT, [_INT, _INT] + [_P] * 8 + [_I64, _P, _P, _P, _P, _P, _P, _P]),
     "bp_bins_cycle": (_INT, [_INT, _INT] + [_P] * 4 + [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _P,

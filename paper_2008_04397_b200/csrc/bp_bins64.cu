@@ -2,14 +2,17 @@
 // precision "double", arithmetic "fast").  Same layout and cycle as the f32
 // path (bp_bins.cu; bins in cell order, sorted after every cycle, no sort
 // phase), with the generic kernel's f64 fast arithmetic so that the result is
-// BITWISE the flat f64 fast path's (bp_fast.cu, FastPolicy<double, double>):
+// BITWISE the flat f64 fast path's (bp_fast.cu f64_split_fused: the split
+// mover, then the generic FastPolicy<double, double> deposit):
 //
 //   mover_bins64    one warp per bin (claims of consecutive bins); each lane
-//                   pushes its particle with FastPolicy::push (kernels.py:
-//                   498-676: trilinear gather of the 8 node records, implicit
-//                   rotation, boundary folds) — a bin's particles share one
-//                   cell, so their node records stay in L1; leavers are listed
-//                   and the holes refilled exactly as in the f32 mover.
+//                   pushes its particle with the split kernels' push
+//                   (sk::push<double>, kernels.py:498-676: the cell's
+//                   coefficient record, 42 DFMA per gather, implicit
+//                   rotation), boundary folds skipped for a warp below the
+//                   bin's speed bound — a bin's particles share one cell, so
+//                   its record stays in L1; leavers are listed and the holes
+//                   refilled exactly as in the f32 mover.
 //   migrate_bins    (bp_bins_plumb.cuh) every leaver to its new bin.
 //   deposit_bins64  one warp per bin, 32-particle tiles staged in shared memory
 //                   (cell check, fractions, moment values once per particle);
@@ -27,13 +30,15 @@
 //                   that keeps f64 within 1e-10 of the reference.
 //   deposit_list64  the overflow and misplaced particles (rare), one at a time.
 //
-// Node records (bp_node_records_build): Ex Ey Ez Bx By Bz invvol 0 per node
-// in f64 (pack_nodes), then max |invvol| in the last 32 bytes — the magic-
-// rint range guard's bound.
+// Field records: the split kernels' per-cell coefficient records in f64
+// (bp_field_records_build, pbytes 8; max |E| in the last 32 bytes).  The
+// deposit reads invvol itself; max |invvol| (the magic-rint range guard's
+// bound) is reduced into the spare stat word 7 at the start of the cycle.
 #include <algorithm>
 #include <cstdint>
 
 #include "bp_bins_plumb.cuh"
+#include "bp_f32_common.cuh"
 #include "bp_fast_policy.cuh"
 #include "bp_launch_impl.cuh"
 
@@ -90,14 +95,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// the bin (x-fastest cell index) of an in-box position: FastPolicy::cell_t's
-// arithmetic (gx = x * (1/dx) - ox/dx, min(trunc(gx), n - 1))
-__device__ __forceinline__ int bin_of(const SP& a, const FastScalars<double>& s, double x,
-                                      double y, double z) {
-  const int i = min((int)fma(x, s.idx(0), -s.ogs(0)), a.nx - 1);
-  const int j = min((int)fma(y, s.idx(1), -s.ogs(1)), a.ny - 1);
-  const int k = min((int)fma(z, s.idx(2), -s.ogs(2)), a.nz - 1);
-  return i + a.nx * j + a.nx * a.ny * k;
+// the bin (x-fastest cell index) of an in-box position: sk::cell_of's
+// arithmetic (gx = x * (1/dx) - ox/dx, min(trunc(gx), n - 1)), which is also
+// FastPolicy::cell_t's
+__device__ __forceinline__ int bin_of(const sk::Params<double>& a, double x, double y,
+                                      double z) {
+  const int i = min((int)fma(x, a.idx[0], -a.ogs[0]), a.nx - 1);
+  const int j = min((int)fma(y, a.idx[1], -a.ogs[1]), a.ny - 1);
+  const int k = min((int)fma(z, a.idx[2], -a.ogs[2]), a.nz - 1);
+  return i + a.nx * j + a.cny * k;
 }
 
 // ---------------------------------------------------------------------------
@@ -108,8 +114,9 @@ __device__ __forceinline__ int bin_of(const SP& a, const FastScalars<double>& s,
 #ifndef BP_MOV64_MINB
 #define BP_MOV64_MINB 5  // resident 128-thread blocks per SM (measured at C2: 4 -> 0.248 ms, 5 -> 0.242, 6 -> 0.256)
 #endif
-__global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(const __grid_constant__ SP a,
-                                                     const __grid_constant__ Bins b) {
+template <bool RX, bool RY, bool RZ>
+__global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(
+    const __grid_constant__ sk::Params<double> a, const __grid_constant__ Bins b) {
   __shared__ unsigned short holes_s[kWarps][kHoleCap];
   __shared__ int lvslot_s[kWarps][kHoleCap];
   const int wid = threadIdx.x >> 5;
@@ -117,7 +124,11 @@ __global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(const __grid
   unsigned short* const holes = holes_s[wid];
   int* const lvslot = lvslot_s[wid];
   const unsigned lt = lanemask_lt();
-  const FastScalars<double> s(a);
+  // the per-bin speed bound below which no position of a push leaves the box
+  // (bp_bins.cu bin_speed_bound, in f64)
+  const double qe = fabs(a.qdt2m) * (double)__ldg(a.emax) * 1.00001;
+  const double hmin = 0.9999 * fmin(fmin(a.L[0] / a.nx, a.L[1] / a.ny), a.L[2] / a.nz);
+  const double epsmax = fmax(fmax(a.bc_eps[0], a.bc_eps[1]), a.bc_eps[2]);
   long long lv_base = 0, lv_next = 0;
   int lv_used = kLvChunk;
   double4 na = make_double4(0, 0, 0, 0), nb = na;
@@ -140,6 +151,10 @@ __global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(const __grid
       }
       if (n > 0) {
         if (!pf_ok && (int)lane < n) ld_rec_stream(b.rec + 2 * (s0 + lane), na, nb);
+        const int ci = c % a.nx, cj = (c / a.nx) % a.ny, ck = c / a.cny;
+        const int cells = min(min(min(ci, a.nx - 1 - ci), min(cj, a.ny - 1 - cj)),
+                              min(ck, a.nz - 1 - ck));
+        const double vmax = (cells * hmin - epsmax) / a.dt - qe;
         int nh = 0;
 #pragma unroll 1
         for (int t0 = 0; t0 < n; t0 += 32) {
@@ -155,9 +170,11 @@ __global__ void __launch_bounds__(kTpb, BP_MOV64_MINB) mover_bins64(const __grid
           }
           int st = ST_OK;
           int dest = c;
+          const bool all_in =
+              __all_sync(0xffffffffu, !valid || fabs(un) + fabs(vn) + fabs(wn) < vmax);
           if (valid) {
-            st = Pol::push(a, s, xp, yp, zp, un, vn, wn);
-            if (st == ST_OK) dest = bin_of(a, s, xp, yp, zp);
+            st = sk::push<double, RX, RY, RZ, false>(a, xp, yp, zp, un, vn, wn, all_in);
+            if (st == ST_OK) dest = bin_of(a, xp, yp, zp);
             else atomicMax(a.status, st);  // not stored (kernels.py:618-621); the cycle raises
           }
           const bool leave = valid && st == ST_OK && dest != c;
@@ -286,7 +303,6 @@ __device__ __forceinline__ double corner_base(double qs, double fx, double fy, d
 __global__ void __launch_bounds__(256) deposit_list64(const __grid_constant__ SP a,
                                                       const __grid_constant__ Bins b) {
   const FastScalars<double> s(a);
-  const double* fn = static_cast<const double*>(a.fnode);
   const long long no = min((long long)b.stat[ST_OVERFLOW], b.ov_cap);
   const long long nl = min((long long)b.stat[ST_LATE], b.late_cap);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -305,7 +321,7 @@ __global__ void __launch_bounds__(256) deposit_list64(const __grid_constant__ SP
     const bool magic = !magic_unsafe(qs * s.qlim, mv[4], mv[7], mv[9], kMagicLimit);
     for (int l = 0; l < 8; ++l) {
       const int node = corner_node(a, key, l);
-      const double bs = corner_base(qs, fx, fy, fz, l, __ldg(fn + (size_t)node * 8 + 6));
+      const double bs = corner_base(qs, fx, fy, fz, l, __ldg(a.invvol + node));
       for (int m = 0; m < 10; ++m) {
         const long long v64 = (long long)(qb(bs, mv[m], magic) - (u64)kMagicBits);
         if (v64) atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + (size_t)m * a.NN + node),
@@ -367,7 +383,6 @@ __global__ void __launch_bounds__(kTpb) deposit_bins64(const __grid_constant__ S
   double* const st = st_s[threadIdx.x >> 5];
   double* const myrow = st + lane * kRowD;
   const FastScalars<double> s(a);
-  const double* fn = static_cast<const double*>(a.fnode);
   for (;;) {
     unsigned long long cc = 0;
     if (lane == 0) cc = atomicAdd(&b.stat[ST_WORK_DEP], (unsigned long long)b.dep_rounds);
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(kTpb) deposit_bins64(const __grid_constant__ S
       const int ci = c % a.nx, cj = (c / a.nx) % a.ny, ck = c / (a.nx * a.ny);
       const int key = (ci * a.NY + cj) * a.NZ + ck;
       const int node = corner_node(a, key, l);
-      const double iv = __ldg(fn + (size_t)node * 8 + 6);
+      const double iv = __ldg(a.invvol + node);
       u64 S[10];
 #pragma unroll
       for (int m = 0; m < 10; ++m) S[m] = 0;
@@ -454,6 +469,22 @@ __global__ void __launch_bounds__(kTpb) deposit_bins64(const __grid_constant__ S
   }
 }
 
+// max |invvol| as the bits of a non-negative double (they order like the
+// values) into *out: the magic-rint guard's bound (pack_nodes computes the same)
+__global__ void __launch_bounds__(256) invvol_max(const double* __restrict__ iv, int NN,
+                                                  unsigned long long* out) {
+  double m = 0.0;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < NN; n += gridDim.x * blockDim.x)
+    m = fmax(m, fabs(iv[n]));
+  unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = v > bits ? v : bits;
+  }
+  if ((threadIdx.x & 31) == 0 && bits) atomicMax(out, bits);
+}
+
 }  // namespace bins64
 
 namespace {
@@ -476,40 +507,33 @@ int resident_blocks(K k, int threads) {
 
 }  // namespace
 
-size_t node_records_bytes(int pbytes, const int64_t* geo_i) {
-  const size_t nn = (size_t)(geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
-  return ((nn * 8 * (pbytes == 8 ? 8 : 4) + 31) & ~(size_t)31) + 32;
-}
-
-int node_records_build(int pbytes, int fbytes, const void* E, const void* B,
-                       const void* invvol, const int64_t* geo_i, void* out, cudaStream_t s) {
-  const size_t bytes = node_records_bytes(pbytes, geo_i);
-  const int NN = (int)((geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1));
-  unsigned long long* ivm = reinterpret_cast<unsigned long long*>((char*)out + bytes - 32);
-  cudaMemsetAsync(ivm, 0, 32, s);
-  const int pb = std::min((NN + 255) / 256, 4096);
-  if (pbytes == 8 && fbytes == 8)
-    pack_nodes<double, double><<<pb, 256, 0, s>>>((const double*)E, (const double*)B,
-                                                  (const double*)invvol, NN, (double*)out, ivm);
-  else if (pbytes == 4 && fbytes == 8)
-    pack_nodes<double, float><<<pb, 256, 0, s>>>((const double*)E, (const double*)B,
-                                                 (const double*)invvol, NN, (float*)out, ivm);
-  else
-    pack_nodes<float, float><<<pb, 256, 0, s>>>((const float*)E, (const float*)B,
-                                                (const float*)invvol, NN, (float*)out, ivm);
+// One cycle of one f64 species on the binned layout (c.records: the f64
+// coefficient records of bp_field_records_build for the current E/B).
+template <bool RX, bool RY, bool RZ>
+int launch_mover64(const sk::Params<double>& ap, const bins64::Bins& b, cudaStream_t s) {
+  auto k = bins64::mover_bins64<RX, RY, RZ>;
+  const int g = resident_blocks(k, bins64::kTpb);
+  bins64::Bins bb = b;
+  // claims sized so that every warp gets several (dynamic claiming balances
+  // the tail)
+  const long long w = (long long)g * bins64::kWarps;
+  bb.move_claim = (int)std::max(1LL, std::min((long long)bins64::kMoveClaim, b.ncell / (6 * w)));
+  const int th = timing_begin(TK_MOVER, s);
+  k<<<g, bins64::kTpb, 0, s>>>(ap, bb);
+  timing_end(th, s);
   note_launch();
-  return check64("node_records_build");
+  return check64("mover_bins64 launch");
 }
 
-// One cycle of one f64 species on the binned layout (c.records: the node
-// records of bp_node_records_build for the current E/B).
 int bins_cycle64(const Call& c0, const BinsArgs& ba, cudaStream_t s) {
   Call c = c0;
   c.apply_bc = 1;
   bins64::SP a = make_params<double, double>(c);
-  a.fnode = c.records;
-  a.iv_max = reinterpret_cast<const double*>((const char*)c.records +
-                                             node_records_bytes(8, c.geo_i) - 32);
+  sk::Params<double> ap;
+  fill_params<double>(c, ap);
+  ap.rec = c.records;
+  ap.emax = reinterpret_cast<const float*>((const char*)c.records +
+                                           split_records_bytes(8, c.geo_i) - 32);
   bins64::Bins b{};
   b.rec = (double4*)ba.rec;
   b.id = (long long*)ba.ids;
@@ -524,17 +548,22 @@ int bins_cycle64(const Call& c0, const BinsArgs& ba, cudaStream_t s) {
   b.late_cap = ba.late_cap;
   b.stat = (unsigned long long*)ba.stat;
   cudaMemsetAsync(b.stat, 0, bins::ST_N * sizeof(unsigned long long), s);
-  // claims sized so that every warp gets several (dynamic claiming balances
-  // the tail)
-  const int gm = resident_blocks(bins64::mover_bins64, bins64::kTpb);
-  const long long wm = (long long)gm * bins64::kWarps;
-  b.move_claim =
-      (int)std::max(1LL, std::min((long long)bins64::kMoveClaim, b.ncell / (6 * wm)));
-  int th = timing_begin(TK_MOVER, s);
-  bins64::mover_bins64<<<gm, bins64::kTpb, 0, s>>>(a, b);
-  timing_end(th, s);
+  // stat word 7: max |invvol| for the deposit's range guard
+  a.iv_max = reinterpret_cast<const double*>(b.stat + 7);
+  bins64::invvol_max<<<std::min((a.NN + 255) / 256, 1024), 256, 0, s>>>(
+      (const double*)c.invvol, a.NN, b.stat + 7);
   note_launch();
-  int rc = check64("mover_bins64 launch");
+  int rc;
+  switch ((c.geo_i[3] ? 1 : 0) | (c.geo_i[4] ? 2 : 0) | (c.geo_i[5] ? 4 : 0)) {
+    case 0: rc = launch_mover64<false, false, false>(ap, b, s); break;
+    case 1: rc = launch_mover64<true, false, false>(ap, b, s); break;
+    case 2: rc = launch_mover64<false, true, false>(ap, b, s); break;
+    case 3: rc = launch_mover64<true, true, false>(ap, b, s); break;
+    case 4: rc = launch_mover64<false, false, true>(ap, b, s); break;
+    case 5: rc = launch_mover64<true, false, true>(ap, b, s); break;
+    case 6: rc = launch_mover64<false, true, true>(ap, b, s); break;
+    default: rc = launch_mover64<true, true, true>(ap, b, s); break;
+  }
   if (rc) return rc;
   bins::migrate_bins<double><<<sm_count() * 8, 256, 0, s>>>(b);
   note_launch();
@@ -542,7 +571,7 @@ int bins_cycle64(const Call& c0, const BinsArgs& ba, cudaStream_t s) {
   const int gd = resident_blocks(bins64::deposit_bins64, bins64::kTpb);
   const long long wd = (long long)gd * bins64::kWarps;
   b.dep_rounds = (int)std::max(1LL, std::min(8LL, b.ncell / (6 * wd)));
-  th = timing_begin(TK_DEPOSIT, s);
+  const int th = timing_begin(TK_DEPOSIT, s);
   bins64::deposit_bins64<<<gd, bins64::kTpb, 0, s>>>(a, b);
   timing_end(th, s);
   note_launch();

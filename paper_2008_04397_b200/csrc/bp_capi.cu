@@ -514,8 +514,9 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
   rc |= cuda_check(cudaMemcpyAsync(h.dinv, invvol, nn * fbytes, cudaMemcpyHostToDevice, s0), "invvol h2d");
   rc |= cuda_check(cudaMemcpyAsync(h.dacc, acc, 10 * nn * 8, cudaMemcpyHostToDevice, s0), "acc h2d");
   rc |= cuda_check(cudaMemsetAsync(h.dstatus, 0, sizeof(int), s0), "status");
-  // f32 fast path: the cell records of E/B once for all batches
-  const bool f32rec = arith == BP_ARITH_FAST && pbytes == 4;
+  // fast path (f32, or f64 with f64 fields): the cell records of E/B once
+  // for all batches
+  const bool f32rec = arith == BP_ARITH_FAST && (pbytes == 4 || fbytes == 8);
   if (f32rec && !rc) {
     const size_t rb = split_records_bytes(pbytes, geo_i) + 256;
     if (rb > h.rec_bytes) {
@@ -690,36 +691,6 @@ int bp_bins_leaver_bytes(int pbytes) {
     return BP_EINVAL;
   }
   return bp::bins_leaver_bytes(pbytes);
-}
-
-int64_t bp_node_records_bytes(int pbytes, const int64_t* geo_i) {
-  if (pbytes != 4 && pbytes != 8) {
-    set_error("particle dtype must be 4 or 8 bytes");
-    return BP_EINVAL;
-  }
-  if (!geo_i || geo_i[0] < 1 || geo_i[1] < 1 || geo_i[2] < 1) {
-    set_error("cell counts must be >= 1");
-    return BP_EINVAL;
-  }
-  return (int64_t)bp::node_records_bytes(pbytes, geo_i);
-}
-
-int bp_node_records_build(int pbytes, int fbytes, const void* E, const void* B,
-                          const void* invvol, const int64_t* geo_i, void* records,
-                          void* stream) {
-  if (!((pbytes == 8 && fbytes == 8) || (pbytes == 4 && (fbytes == 4 || fbytes == 8)))) {
-    set_error("unsupported dtype pair (particles %d bytes, fields %d bytes)", pbytes, fbytes);
-    return BP_EINVAL;
-  }
-  if (!E || !B || !invvol || !records || !geo_i || geo_i[0] < 1 || geo_i[1] < 1 ||
-      geo_i[2] < 1 || ((uintptr_t)records % 32) != 0) {
-    set_error("node_records_build: E, B, invvol, geo_i and 32-byte aligned records required");
-    return BP_EINVAL;
-  }
-  return bp::node_records_build(pbytes, fbytes, E, B, invvol, geo_i, records,
-                                (cudaStream_t)stream)
-             ? BP_ECUDA
-             : BP_OK;
 }
 
 int bp_bins_plan(int pbytes, int fbytes, const void* xs, const void* ys, const void* zs, int64_t n,

@@ -156,6 +156,87 @@ __device__ __forceinline__ void tri_pair(const double4& A, const double4& B, con
            fma(fma(B.w, fx, B.y), fy, fma(A.w, fx, A.y)));
 }
 
+
+// The implicit push of the fast kernels (kernels.py:498-676) on the per-cell
+// coefficient records: the flat split mover (bp_split.cu, f32) and the f64
+// binned mover (bp_bins64.cu).
+// skipbc (warp-uniform): the caller has shown that no position of this push
+// can leave the box (interior()), so the boundary folds and checks are
+// identities and are skipped.
+template <typename T, bool RX, bool RY, bool RZ, bool REUSE>
+__device__ __forceinline__ int push(const Params<T>& a, T& xp, T& yp, T& zp, T& un, T& vn,
+                                    T& wn, bool skipbc) {
+  typedef typename Quad<T>::type Q;
+  T vbx = un, vby = vn, vbz = wn;
+  Q R[12];
+  int held = -1;  // cell whose record is in R
+#pragma unroll 1
+  for (int it = 0; it < a.n_iters; ++it) {
+    T xm, ym;
+    if constexpr (std::is_same<T, float>::value) {
+      const F2 XM = fma2(f2(vbx, vby), f2(a.dth, a.dth), f2(xp, yp));
+      xm = XM.x;
+      ym = XM.y;
+    } else {
+      xm = fma(vbx, a.dth, xp);
+      ym = fma(vby, a.dth, yp);
+    }
+    T zm = fma(vbz, a.dth, zp);
+    if (!skipbc) {
+      xm = fold_mid<RX>(xm, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+      ym = fold_mid<RY>(ym, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+      zm = fold_mid<RZ>(zm, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+      if (xm < a.o[0] || xm > a.hi[0] || ym < a.o[1] || ym > a.hi[1] || zm < a.o[2] ||
+          zm > a.hi[2])
+        return ST_MIDPOINT;
+    }
+    T fx, fy, fz;
+    int i, j, k;
+    const int cell = cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    if (!REUSE || cell != held) {
+      held = cell;
+      const Q* r = static_cast<const Q*>(a.rec) + (size_t)cell * 12;
+#pragma unroll
+      for (int q = 0; q < 12; q += 2) ldg_pair(r + q, R[q], R[q + 1]);
+    }
+    T ex, ey, hx, hy, ez, hz;
+    tri_pair(R[0], R[1], R[2], R[3], fx, fy, fz, ex, ey);
+    tri_pair(R[4], R[5], R[6], R[7], fx, fy, fz, hx, hy);
+    tri_pair(R[8], R[9], R[10], R[11], fx, fy, fz, ez, hz);
+    T tx, ty;
+    if constexpr (std::is_same<T, float>::value) {
+      const F2 Txy = fma2(f2(a.qdt2m, a.qdt2m), f2(ex, ey), f2(un, vn));
+      tx = Txy.x;
+      ty = Txy.y;
+    } else {
+      tx = fma(a.qdt2m, ex, un);
+      ty = fma(a.qdt2m, ey, vn);
+    }
+    const T tz = fma(a.qdt2m, ez, wn);
+    const T bsq = fma(hx, hx, fma(hy, hy, hz * hz));
+    const T inv = rcp_fast(fma(a.beta2, bsq, T(1)));
+    const T tdb = fma(tx, hx, fma(ty, hy, tz * hz));
+    const T bt = a.beta * tdb;
+    const T cx = fma(ty, hz, -tz * hy), cy = fma(tz, hx, -tx * hz), cz = fma(tx, hy, -ty * hx);
+    vbx = fma(a.beta, fma(bt, hx, cx), tx) * inv;
+    vby = fma(a.beta, fma(bt, hy, cy), ty) * inv;
+    vbz = fma(a.beta, fma(bt, hz, cz), tz) * inv;
+  }
+  T xo = fma(vbx, a.dt, xp), yo = fma(vby, a.dt, yp), zo = fma(vbz, a.dt, zp);
+  T uo = T(2) * vbx - un, vo = T(2) * vby - vn, wo = T(2) * vbz - wn;
+  if (!skipbc) {
+    fold_commit<RX>(xo, uo, a.o[0], a.L[0], a.hi[0], a.hi2[0]);
+    fold_commit<RY>(yo, vo, a.o[1], a.L[1], a.hi[1], a.hi2[1]);
+    fold_commit<RZ>(zo, wo, a.o[2], a.L[2], a.hi[2], a.hi2[2]);
+    if (xo < a.o[0] || xo > a.hi[0] || yo < a.o[1] || yo > a.hi[1] || zo < a.o[2] ||
+        zo > a.hi[2])
+      return ST_RUNAWAY;
+  }
+  xp = xo; yp = yo; zp = zo;
+  un = uo; vn = vo; wn = wo;
+  return ST_OK;
+}
+
 }  // namespace sk
 
 struct Call;

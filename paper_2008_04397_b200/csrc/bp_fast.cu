@@ -21,18 +21,42 @@ int dispatch(const Call& c, cudaStream_t s) {
   return -1;
 }
 
+// f64 fused span: the split mover (coefficient records, interior skip;
+// bp_split.cu) then the generic per-contribution deposit over the particles
+// whose push succeeded — the arithmetic of the f64 binned path
+// (bp_bins64.cu), which is bitwise this one
+int f64_split_fused(const Call& c0, cudaStream_t s) {
+  Call c = c0;
+  const size_t skip_bytes = (((size_t)c.count + 31) / 32 * 4 + 8 + 255) & ~(size_t)255;
+  unsigned* skip = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&skip, skip_bytes, s);
+  if (e != cudaSuccess) {
+    set_error("skip bitmask alloc: %s", cudaGetErrorString(e));
+    return -2;
+  }
+  cudaMemsetAsync(skip, 0, skip_bytes, s);
+  c.skip = skip;
+  c.apply_bc = 1;
+  int rc = split_push_f64(c, c.records, skip, s);
+  if (!rc) rc = run_span<FastPolicy<double, double>, false, true>(c, true, s);
+  cudaFreeAsync(skip, s);
+  return rc;
+}
+
 }  // namespace
 
 int launch_fast(const Call& c, cudaStream_t s) {
-  // f32 particles, fused: the mover + deposit kernels of bp_split.cu
-  // (BP_FAST_GENERIC=1 selects the generic policy kernel instead).  f64 stays
-  // on the generic kernel: its per-contribution rint keeps the moments within
-  // 1e-10 of the reference's lattice, which per-tile f64 sums do not (the
-  // reference's own rounding noise is ~1e-10 of the small pressure moments).
-  if (c.op == OP_FUSED && c.pbytes == 4) {
-    const char* env = getenv("BP_FAST_GENERIC");
-    if (!(env && env[0] == '1')) return split_fused(c, c.records, s);
-  }
+  // f32 particles, fused: the mover + deposit kernels of bp_split.cu; f64,
+  // fused: the split mover + the generic deposit, whose per-contribution rint
+  // keeps the moments within 1e-10 of the reference's lattice (per-tile f64
+  // sums do not: the reference's own rounding noise is ~1e-10 of the small
+  // pressure moments).  BP_FAST_GENERIC=1 selects the generic policy kernel
+  // for both.
+  const char* env = getenv("BP_FAST_GENERIC");
+  const bool generic = env && env[0] == '1';
+  if (c.op == OP_FUSED && c.pbytes == 4 && !generic) return split_fused(c, c.records, s);
+  if (c.op == OP_FUSED && c.pbytes == 8 && c.fbytes == 8 && !generic)
+    return f64_split_fused(c, s);
   if (c.pbytes == 8 && c.fbytes == 8) return dispatch<double, double>(c, s);
   if (c.pbytes == 4 && c.fbytes == 4) return dispatch<float, float>(c, s);
   if (c.pbytes == 4 && c.fbytes == 8) return dispatch<float, double>(c, s);

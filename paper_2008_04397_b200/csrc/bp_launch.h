@@ -43,6 +43,8 @@ size_t split_records_bytes(int pbytes, const int64_t* geo_i);
 int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
                        const int64_t* geo_i, void* rec, cudaStream_t s);
 int split_fused(const Call& c, const void* rec, cudaStream_t s);
+// the f64 fast fused span's mover pass (bp_split.cu) with the failed-push bitmask
+int split_push_f64(const Call& c, const void* rec, unsigned* skip, cudaStream_t s);
 
 // Cell-binned f32 fast path (bp_bins.cu): the bin layout of one species
 struct BinsArgs {
@@ -63,11 +65,7 @@ struct BinsArgs {
 int bins_leaver_bytes(int pbytes);
 int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s);
 int bins_cycle64(const Call& c, const BinsArgs& ba, cudaStream_t s);  // bp_bins64.cu
-// node records of the generic fast arithmetic (pack_nodes: Ex Ey Ez Bx By Bz
-// invvol 0 per node, then max |invvol| in the last 32 bytes)
-size_t node_records_bytes(int pbytes, const int64_t* geo_i);
-int node_records_build(int pbytes, int fbytes, const void* E, const void* B, const void* invvol,
-                       const int64_t* geo_i, void* out, cudaStream_t s);
+
 int bins_plan(const Call& c, int* count, int64_t* start, double frac, int smin, int64_t* total,
               cudaStream_t s);
 int bins_fill(const Call& c, const int64_t* src_ids, const int64_t* start, void* dst_rec,

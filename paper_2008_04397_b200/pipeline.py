@@ -150,20 +150,16 @@ class DeviceSimulation:
         self.mixed = 1 if npd != nfd else 0
         self.scale = float(nfd(MOMENT_SCALE))
         self._arith = {"parity": _lib.ARITH_PARITY, "fast": _lib.ARITH_FAST}[self.arith]
-        # f32 fast path: per-cell field records (bp_field_records_build); f64
-        # binned: node records (bp_node_records_build) — built once per field
-        # update and shared by every species' call
+        # fast arithmetic: per-cell coefficient records of E/B in the particle
+        # precision (bp_field_records_build), built once per field update and
+        # shared by every species' call (f32, mixed, and f64 with f64 fields)
         self.records = None
-        self._records_kind = None
         self._records_fresh = False
-        gi = np.ascontiguousarray(self.geo_i, np.int64)
-        if self.arith == "fast" and pd == torch.float32:
-            nbytes = int(_lib.load().bp_field_records_bytes(4, ctypes.c_void_p(gi.ctypes.data)))
-            self._records_kind = "cells"
-        elif self.binned:
-            nbytes = int(_lib.load().bp_node_records_bytes(8, ctypes.c_void_p(gi.ctypes.data)))
-            self._records_kind = "nodes"
-        if self._records_kind is not None:
+        self._records_pbytes = 4 if pd == torch.float32 else 8
+        if self.arith == "fast":
+            gi = np.ascontiguousarray(self.geo_i, np.int64)
+            nbytes = int(_lib.load().bp_field_records_bytes(self._records_pbytes,
+                                                            ctypes.c_void_p(gi.ctypes.data)))
             self.records = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=self.device)
         if self.reduce not in ("all", "root"):
             raise ConfigurationError(f"reduce must be 'all' or 'root', not {self.reduce!r}")
@@ -261,9 +257,8 @@ class DeviceSimulation:
         self._records_fresh = False
 
     def _records_ptr(self, stream):
-        """Device address of the cell (f32 fast) or node (f64 binned) records
-        for the current E/B (built on first use after a field update), or
-        None where the kernels build their own."""
+        """Device address of the cell records for the current E/B (built on
+        first use after a field update), or None off the fast arithmetic."""
         if self.records is None:
             return None
         base = self.records.data_ptr()
@@ -271,22 +266,12 @@ class DeviceSimulation:
         if not self._records_fresh:
             L = _lib.load()
             gi = np.ascontiguousarray(self.geo_i, np.int64)
-            if self._records_kind == "cells":
-                rc = L.bp_field_records_build(4, self.E.element_size(),
-                                              ctypes.c_void_p(self.E.data_ptr()),
-                                              ctypes.c_void_p(self.B.data_ptr()),
-                                              ctypes.c_void_p(gi.ctypes.data),
-                                              ctypes.c_void_p(ptr),
-                                              ctypes.c_void_p(stream.cuda_stream))
-                _lib.check(rc, "field_records_build")
-            else:
-                rc = L.bp_node_records_build(8, 8, ctypes.c_void_p(self.E.data_ptr()),
-                                             ctypes.c_void_p(self.B.data_ptr()),
-                                             ctypes.c_void_p(self.invvol.data_ptr()),
-                                             ctypes.c_void_p(gi.ctypes.data),
-                                             ctypes.c_void_p(ptr),
-                                             ctypes.c_void_p(stream.cuda_stream))
-                _lib.check(rc, "node_records_build")
+            rc = L.bp_field_records_build(self._records_pbytes, self.E.element_size(),
+                                          ctypes.c_void_p(self.E.data_ptr()),
+                                          ctypes.c_void_p(self.B.data_ptr()),
+                                          ctypes.c_void_p(gi.ctypes.data), ctypes.c_void_p(ptr),
+                                          ctypes.c_void_p(stream.cuda_stream))
+            _lib.check(rc, "field_records_build")
             self._records_fresh = True
         return ptr
 
