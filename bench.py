@@ -469,6 +469,30 @@ def main_ours(args):
         del psim, pt
         torch.cuda.empty_cache()
 
+    # the same workload with the species on two streams (BP_BIN_STREAMS=2:
+    # one species' deposit shares the SMs with the next one's mover); kept
+    # out of the headline so that its per-kernel event times (the roofline)
+    # are not inflated by the overlap
+    if sim.binned and world == 1:
+        os.environ["BP_BIN_STREAMS"] = "2"
+        try:
+            for _ in range(2):
+                sim.run_cycle()
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockMonitor(local_dev) as mon2:
+                b0.record()
+                for _ in range(args.steps):
+                    sim.run_cycle()
+                b1.record()
+                torch.cuda.synchronize()
+            extra["bin_streams_2"] = {"value": n_total * args.steps / (b0.elapsed_time(b1) * 1e-3),
+                                      "unit": UNIT, "steps": args.steps,
+                                      "ms_per_step": b0.elapsed_time(b1) / args.steps,
+                                      "clocks": mon2.summary()}
+        finally:
+            os.environ.pop("BP_BIN_STREAMS", None)
+
     # BASELINE configs[1] (C2, 2D GEM 256 x 128 x 1, f64): the binned f64 fast
     # path, the flat generic f64 fast path and the bitwise arithmetic, with
     # their own clocks (one GPU; skipped when the headline already is f64)

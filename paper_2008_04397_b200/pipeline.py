@@ -199,6 +199,7 @@ class DeviceSimulation:
         if (self._lists is None or self._lists.pbytes != pb
                 or self._lists.leaver_cap < int(n_max * 0.25) + (1 << 20)):
             self._lists = TransitLists(self.device, n_max, pbytes=pb)
+            self._side_lists = None
 
     @property
     def particles(self):
@@ -293,13 +294,21 @@ class DeviceSimulation:
         _lib.check(rc, "fused_span")
 
     def _side_streams(self, s):
-        """Species on alternating side streams (env BP_SPECIES_STREAMS=2):
-        one species' deposit may then share the SMs with the next one's
-        mover.  The side streams start after everything queued on `s`."""
+        """Species on alternating side streams (env BP_SPECIES_STREAMS=2 on
+        the flat layout, BP_BIN_STREAMS=2 on the bins, each stream with its
+        own leaver list): one species' deposit may then share the SMs with
+        the next one's mover.  The side streams start after everything
+        queued on `s`."""
         import os
-        n = int(os.environ.get("BP_SPECIES_STREAMS", "0"))
+        n = int(os.environ.get("BP_BIN_STREAMS" if self.binned else "BP_SPECIES_STREAMS", "0"))
         if n <= 1:
             return []
+        if self.binned and (getattr(self, "_side_lists", None) is None
+                            or len(self._side_lists) != n):
+            from .bins import TransitLists
+            n_max = max(b.n for b in self._bins if b is not None)
+            self._side_lists = [TransitLists(self.device, n_max, pbytes=self._lists.pbytes)
+                                for _ in range(n)]
         torch = self.torch
         if getattr(self, "_side", None) is None or len(self._side) != n:
             self._side = [torch.cuda.Stream(device=self.device) for _ in range(n)]
@@ -322,7 +331,7 @@ class DeviceSimulation:
         # the cell records are built on `s` before any side stream forks off
         # it (side streams wait on everything queued on `s` so far)
         rec = self._records_ptr(s)
-        side = [] if self.binned else self._side_streams(s)
+        side = self._side_streams(s)
         self._flat_cache = None
         for sid, n in enumerate(self._species_n()):
             if n == 0:
@@ -330,8 +339,10 @@ class DeviceSimulation:
             ss = side[sid % len(side)] if side else s
             if self.binned:
                 sp = self.species[sid]
-                self._bins[sid].cycle(self._lists, rec, self.acc[sid], self.invvol,
-                                      self.scalars[sid], sp.mover_iters, self.scale, self.status, s)
+                lists = self._side_lists[sid % len(side)] if side else self._lists
+                self._bins[sid].cycle(lists, rec, self.acc[sid], self.invvol,
+                                      self.scalars[sid], sp.mover_iters, self.scale, self.status,
+                                      ss)
             else:
                 for (b0, bn) in partition_batches(n, self.batches).spans:
                     if bn:
