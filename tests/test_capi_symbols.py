@@ -62,3 +62,26 @@ def test_ctypes_signatures_match_header():
     assert set(counts) == set(_lib.EXPORTS)
     for name, (_res, argtypes) in _lib._SIGS.items():
         assert len(argtypes) == counts[name], (name, len(argtypes), counts[name])
+
+
+def test_bins_abi_argument_checks_without_gpu():
+    """The binned layout's entry points validate their dtype arguments before
+    any CUDA call: 48- / 80-byte leaver records for f32 / f64 particles, and
+    only the (4, 4), (4, 8), (8, 8) particle / field pairs."""
+    import numpy as np
+    from paper_2008_04397_b200 import _lib
+    L = _lib.load()
+    assert L.bp_bins_leaver_bytes(4) == 48
+    assert L.bp_bins_leaver_bytes(8) == 80
+    assert L.bp_bins_leaver_bytes(2) == _lib.EINVAL
+    gi = np.array([4, 4, 4, 0, 1, 0], np.int64)
+    gg = np.zeros(6, np.float64)
+    gf = np.zeros(9, np.float64)
+    p = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    total = ctypes.c_int64(0)
+    rc = L.bp_bins_plan(8, 4, None, None, None, 0, p(gf), p(gg), p(gi), 1.0, 64, None, None,
+                        ctypes.byref(total), None)
+    assert rc == _lib.EINVAL and b"binned layout" in L.bp_last_error()
+    rc = L.bp_bins_export(3, None, None, None, None, 64, None, 0, None, None, None, None,
+                          ctypes.byref(total), None)
+    assert rc == _lib.EINVAL
