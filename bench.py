@@ -78,6 +78,8 @@ def parse():
     ap.add_argument("--no-shuffled", action="store_true")
     ap.add_argument("--no-c2-double", action="store_true",
                     help="skip the C2 f64 leg (extra.c2_double)")
+    ap.add_argument("--no-streams-leg", action="store_true",
+                    help="skip the two-stream leg (extra.bin_streams_2)")
     ap.add_argument("--bin-slack", default=None,
                     help="binned layout headroom 'frac,min' (DeviceSimulation.bin_slack)")
     return ap.parse_args()
@@ -114,13 +116,15 @@ def peaks():
 
 
 def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    summary (profiles/ncu_summary_r02b.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary_r02b.json")) as f:
-            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """DRAM bytes per launch of `kernel` from the newest committed ncu capture
+    summary that has it (profiles/ncu_summary_r02e.json, then r02b), or None."""
+    for tag in ("r02e", "r02b"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json")) as f:
+                return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+        except Exception:
+            continue
+    return None
 
 
 class ClockMonitor:
@@ -473,7 +477,7 @@ def main_ours(args):
     # one species' deposit shares the SMs with the next one's mover); kept
     # out of the headline so that its per-kernel event times (the roofline)
     # are not inflated by the overlap
-    if sim.binned and world == 1:
+    if sim.binned and world == 1 and not args.no_streams_leg:
         os.environ["BP_BIN_STREAMS"] = "2"
         try:
             for _ in range(2):

@@ -102,10 +102,11 @@ class DeviceSimulation:
     layout: str = "auto"
     # bin capacity = count + max(slack[1], slack[0] * count), rounded to 8
     # slots: a bin that fills up forces a re-slack of the species (a copy of
-    # all bins, ~3 ms at C3); bins near the sheet gain ~5 particles per
-    # cycle, and doubling the capacity keeps re-slacks to a few per hundred
-    # cycles (memory: 2 buffer sets x 2 x 40 B per particle)
-    bin_slack: tuple = (1.0, 64)
+    # all bins, ~1.6 ms at C3).  None: the largest of slack fractions 3, 2, 1
+    # (min 64) whose two buffer sets fit half the device — at C3 3.0 (86 GB):
+    # over 100 cycles 1 re-slack per electron species instead of 7 with 1.0
+    # (26.3 against 25.8 G particles/s)
+    bin_slack: tuple = None
 
     def __post_init__(self):
         import torch
@@ -132,6 +133,17 @@ class DeviceSimulation:
             raise ConfigurationError(f"layout must be auto, flat or bins, not {self.layout!r}")
         if self.layout == "bins" and not binnable:
             raise ConfigurationError("the binned layout needs the fast arithmetic")
+        if self.bin_slack is None:
+            from .bins import layout_bytes
+            half = 0.5 * torch.cuda.get_device_properties(self.device).total_memory
+            pbytes = 4 if pd == torch.float32 else 8
+            world = self._world_hint()
+            ppcs = [sp.ppc for sp in self.species]
+            self.bin_slack = (1.0, 64)
+            for frac in (3.0, 2.0):
+                if layout_bytes(int(self.geom.n_cells), ppcs, (frac, 64), pbytes, world) <= half:
+                    self.bin_slack = (frac, 64)
+                    break
         if self.layout == "auto" and binnable:
             # the bins hold two buffer sets (live + the re-slack's destination)
             # of (1 + slack) slots per particle: decks whose sets would not fit
@@ -169,14 +181,17 @@ class DeviceSimulation:
         else:
             self.rank, self.world = 0, 1
 
+    def _world_hint(self):
+        if not self.distributed:
+            return 1
+        import torch.distributed as dist
+        return dist.get_world_size(self.group)
+
     def bins_bytes_estimate(self, world=None):
         """Device bytes of the binned layout for this deck on one rank
         (bins.layout_bytes)."""
         if world is None:
-            world = 1
-            if self.distributed:
-                import torch.distributed as dist
-                world = dist.get_world_size(self.group)
+            world = self._world_hint()
         from .bins import layout_bytes
         pbytes = 4 if self.pdt == self.torch.float32 else 8
         return layout_bytes(int(self.geom.n_cells), [sp.ppc for sp in self.species],
