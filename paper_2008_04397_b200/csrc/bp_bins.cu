@@ -653,9 +653,12 @@ __global__ void __launch_bounds__(256) deposit_list(const __grid_constant__ P a,
 #ifndef BP_DEP_UNR
 #define BP_DEP_UNR 4    // particles per lane and iteration (loads in flight)
 #endif
-__global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __grid_constant__ P a,
-                                                                        const __grid_constant__ Bins b) {
-  extern __shared__ __align__(16) float dsm[];
+// CHK: some particle may sit in a bin that is not its cell (the mover
+// counted misplaced ones this cycle): test each against the bin's cell box.
+// Without misplaced particles the test — and the per-bin box it needs, which
+// the register allocator otherwise rematerialises per particle — is skipped.
+template <bool CHK>
+__device__ __forceinline__ void deposit_bins_body(const P& a, const Bins& b, float* dsm) {
   const unsigned lane = threadIdx.x & 31;
   const int qd = (int)(lane >> 3), l = (int)(lane & 7);
   float* const ws = dsm + (threadIdx.x >> 5) * kWarpSm;
@@ -670,12 +673,12 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
     for (int k = 0; k < 7; ++k) n1[u][k] = 0.f;
   // the U particles q, q + 8, ... of this lane (those < lim): one 256-bit
   // read-only load each
-  auto fetch = [&](long long q0, int i0, int lim) {
+  auto fetch = [&](int q0, int i0, int lim) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (i0 + 8 * u < lim) {
         float4 ra, rb;
-        ld_rec_ro(b.rec + 2 * (q0 + 8 * u), ra, rb);
+        ld_rec_ro(slot_rec(b.rec, q0 + 8 * u), ra, rb);
         n1[u][0] = ra.x; n1[u][1] = ra.y; n1[u][2] = ra.z; n1[u][3] = ra.w;
         n1[u][4] = rb.x; n1[u][5] = rb.y; n1[u][6] = rb.z;
       }
@@ -690,11 +693,11 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
     // this quarter's bin of round 0 and its cell coordinates
     int c = c0 + qd;
     Ijk q3 = ijk_of(a, min(c, b.ncell - 1));
-    long long s0 = 0;
+    int s0 = 0;
     int n = 0;
     if (c < b.ncell) {
-      s0 = b.start[c];
-      n = (int)min((long long)b.count[c], b.start[c + 1] - s0);
+      s0 = (int)b.start[c];
+      n = min(b.count[c], (int)b.start[c + 1] - s0);
     }
     fetch(s0 + l, l, n);
 #pragma unroll 1
@@ -703,16 +706,16 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
       const bool okb = c < b.ncell;
       // next round's bin of this quarter
       const int cn = c + 4;
-      long long s1 = 0;
+      int s1 = 0;
       int n_1 = 0;
       if (rnd + 1 < b.dep_rounds && cn < b.ncell) {
-        s1 = b.start[cn];
-        n_1 = (int)min((long long)b.count[cn], b.start[cn + 1] - s1);
+        s1 = (int)b.start[cn];
+        n_1 = min(b.count[cn], (int)b.start[cn + 1] - s1);
       }
       const int nit =
           (int)__reduce_max_sync(0xffffffffu, (unsigned)((n + 8 * U - 1) / (8 * U)));
       if (nit == 0) fetch(s1 + l, l, n_1);  // (the loop below prefetches otherwise)
-      const Box bx = cell_box(a, q3);
+      const float cfx = (float)q3.i, cfy = (float)q3.j, cfz = (float)q3.k;
       F2 A[10][4];
 #pragma unroll
       for (int k = 0; k < 10; ++k)
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
           const float gx = fmaf(xp, a.idx[0], -a.ogs[0]);
           const float gy = fmaf(yp, a.idx[1], -a.ogs[1]);
           const float gz = fmaf(zp, a.idx[2], -a.ogs[2]);
-          if (valid && !in_box(bx, gx, gy, gz)) {
+          if (CHK && valid && !in_box(cell_box(a, q3), gx, gy, gz)) {
             // misplaced (a leaver the mover could not list): the late list
             const unsigned long long o = atomicAdd(&b.stat[ST_LATE], 1ULL);
             if ((long long)o < b.late_cap) {
@@ -752,7 +755,7 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
             valid = false;
           }
           const float qs = valid ? qp : 0.f;
-          const float fx = gx - bx.cf[0], fy = gy - bx.cf[1], fz = gz - bx.cf[2];
+          const float fx = gx - cfx, fy = gy - cfy, fz = gz - cfz;
           const F2 Q = f2(qs - qs * fx, qs * fx);  // q (1 - fx), q fx
           const F2 Qy0 = __fmul2_rn(Q, f2(1.f - fy, 1.f - fy));
           const F2 Qy1 = __fmul2_rn(Q, f2(fy, fy));
@@ -809,6 +812,17 @@ __global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __
       n = n_1;
     }
   }
+}
+
+// Both variants are launched; the one the mover's misplaced count (this
+// stream, an earlier kernel) does not select returns at once — separate
+// kernels keep the checked variant's registers out of the common one.
+template <bool CHK>
+__global__ void __launch_bounds__(BP_DEP_TPB, BP_DEP_MINB) deposit_bins(const __grid_constant__ P a,
+                                                                        const __grid_constant__ Bins b) {
+  extern __shared__ __align__(16) float dsm[];
+  if ((__ldg(b.stat + ST_MISPLACED) != 0ULL) != CHK) return;
+  deposit_bins_body<CHK>(a, b, dsm);
 }
 
 }  // namespace bins
@@ -905,16 +919,21 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   if ((rc = bcheck("migrate_bins launch"))) return rc;
   const size_t smem = (size_t)(BP_DEP_TPB / 32) * bins::kWarpSm * sizeof(float);
   static bool attr[64] = {};
-  if (first_on_device(attr))
-    cudaFuncSetAttribute(bins::deposit_bins, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(bins::deposit_bins<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  const int g = resident_grid(bins::deposit_bins, smem, BP_DEP_TPB);
+    cudaFuncSetAttribute(bins::deposit_bins<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  }
+  const int g = resident_grid(bins::deposit_bins<false>, smem, BP_DEP_TPB);
   b.dep_rounds = (int)std::max(
       1LL, std::min((long long)bins::kDepClaim / 4,
                     (long long)b.ncell / (24LL * g * (BP_DEP_TPB / 32))));
   const int th = timing_begin(TK_DEPOSIT, s);
-  bins::deposit_bins<<<g, BP_DEP_TPB, smem, s>>>(a, b);
+  bins::deposit_bins<false><<<g, BP_DEP_TPB, smem, s>>>(a, b);
+  bins::deposit_bins<true><<<g, BP_DEP_TPB, smem, s>>>(a, b);
   timing_end(th, s);
+  note_launch();
   note_launch();
   if ((rc = bcheck("deposit_bins launch"))) return rc;
   bins::deposit_list<<<nsm(), 256, 0, s>>>(a, b);

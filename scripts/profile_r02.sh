@@ -10,8 +10,11 @@ mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches_$R.csv \
     python bench.py --steps 6 --warmup 0 --no-e2e --no-cpu --no-parity --no-shuffled --no-c2-double --no-streams-leg > gpurun_out/launches_$R.log 2>&1
-for K in mover_bins deposit_bins migrate_bins; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 8 -c 1 \
+# deposit_bins is two template kernels (the misplaced-check variant returns at
+# once when the mover found none): select the common one by mangled name
+for K in mover_bins deposit_binsILb0 migrate_bins; do
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+      -k regex:$K -s 8 -c 1 \
       -o gpurun_out/${K}_$R python bench.py --steps 4 --warmup 0 --no-e2e --no-cpu --no-parity --no-shuffled \
       --no-c2-double --no-streams-leg \
       > gpurun_out/${K}_$R.log 2>&1
