@@ -431,7 +431,14 @@ def main_ours(args):
         "achieved_gbs": per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9,
         "frac": per_launch_particles * bpp / (launch_ms * 1e-3) / 1e9 / hbm}
 
-    extra = {"phase3_kernel_ms_per_step": kern_ms / args.steps,
+    # per-cycle phase-3 device time (the reference's metric: N / phase-3
+    # seconds, median and mean +- stddev over the cycles)
+    p3 = np.array([t.phase3_ms for t in timed], np.float64)
+    extra_p3 = {"median_ms": float(np.median(p3)), "mean_ms": float(p3.mean()),
+                "std_ms": float(p3.std()),
+                "rank0_particles_per_s_median": n_local / (float(np.median(p3)) * 1e-3)}
+    extra = {"phase3_per_cycle": extra_p3,
+             "phase3_kernel_ms_per_step": kern_ms / args.steps,
              "sort_ms_per_sort": sort_ms / max(1, sum(t.sorted_this_cycle for t in timed)),
              "phase3_particles_per_s": n_total / (kern_ms / args.steps * 1e-3)}
     if sim.binned:
