@@ -297,3 +297,24 @@ def test_bins64_c2_fullsize_bitwise(gpu):
         da, db = _by_id(pa), _by_id(pb)
         for k in da:
             assert np.array_equal(da[k], db[k]), k
+
+
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_bins_two_streams_match_one(gpu, label, monkeypatch):
+    """BP_BIN_STREAMS=2 (species on two streams, each with its own leaver
+    list): the particles bitwise those of the one-stream cycle, the moments
+    within the f32 tolerance (f64: bitwise)."""
+    geom, species, prec, bufs, fields = _gem(label=label)
+    a = _sim(geom, species, prec, bufs, "bins")
+    b = _sim(geom, species, prec, bufs, "bins")
+    for cyc in range(4):
+        monkeypatch.setenv("BP_BIN_STREAMS", "2")
+        a.run_cycle(fields.E, fields.B)
+        monkeypatch.delenv("BP_BIN_STREAMS")
+        b.run_cycle(fields.E, fields.B)
+        _assert_moments_close(b.moments_host(), a.moments_host(), _tol(label))
+    assert a._side_lists is not None and len(a._side_lists) == 2
+    for pa, pb in zip(a.particles, b.particles):
+        da, db = _by_id(pa), _by_id(pb)
+        for k in da:
+            assert np.array_equal(da[k], db[k]), k
