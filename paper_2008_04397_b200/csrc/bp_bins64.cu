@@ -1,8 +1,8 @@
 // Cell-binned fast path for f64 particles (DeviceSimulation layout "bins",
 // precision "double", arithmetic "fast").  Same layout and cycle as the f32
 // path (bp_bins.cu; bins in cell order, sorted after every cycle, no sort
-// phase), with the generic kernel's f64 fast arithmetic so that the result is
-// BITWISE the flat f64 fast path's (bp_fast.cu f64_split_fused: the split
+// phase), with the f64 fast arithmetic of the flat path, so that the result
+// is BITWISE the flat f64 fast path's (bp_fast.cu f64_split_fused: the split
 // mover, then the generic FastPolicy<double, double> deposit):
 //
 //   mover_bins64    one warp per bin (claims of consecutive bins); each lane
