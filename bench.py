@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--sort-period", type=int, default=10)
     ap.add_argument("--layout", default="auto", choices=("auto", "flat", "bins"),
                     help="particle layout of the device path (pipeline.DeviceSimulation)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
