@@ -919,12 +919,12 @@ int bins_cycle(const Call& c, const BinsArgs& ba, cudaStream_t s) {
   if ((rc = bcheck("migrate_bins launch"))) return rc;
   const size_t smem = (size_t)(BP_DEP_TPB / 32) * bins::kWarpSm * sizeof(float);
   static bool attr[64] = {};
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(bins::deposit_bins<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaFuncSetAttribute(bins::deposit_bins<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  }
+  });
   const int g = resident_grid(bins::deposit_bins<false>, smem, BP_DEP_TPB);
   b.dep_rounds = (int)std::max(
       1LL, std::min((long long)bins::kDepClaim / 4,

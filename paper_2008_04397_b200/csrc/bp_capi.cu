@@ -252,8 +252,31 @@ struct HostCtx {
   int* dstatus = nullptr;
   int* hstatus = nullptr;
 };
+// One pipeline (streams, slots, field and accumulator buffers) per concurrent
+// call: the reference calls fused_span concurrently from a thread pool on
+// disjoint spans with private accumulators (pipeline.py:164-165, 255-257), and
+// those calls then overlap on the device — one call's pipeline fill and drain
+// under another's steady state.  A call borrows a free pipeline (or makes
+// one) and returns it; pipelines live for the process, like the runtime's
+// own pools, so no CUDA call runs at thread or process exit.
 static std::mutex g_host_mu;
-static HostCtx g_host;
+static std::vector<HostCtx*> g_host_free;
+struct HostLease {
+  HostCtx* h;
+  HostLease() {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    if (g_host_free.empty()) {
+      h = new HostCtx();
+    } else {
+      h = g_host_free.back();
+      g_host_free.pop_back();
+    }
+  }
+  ~HostLease() {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    g_host_free.push_back(h);
+  }
+};
 
 int host_ctx_reserve(HostCtx& h, size_t slot_bytes, size_t field_bytes, size_t acc_bytes) {
   int dev = 0;
@@ -499,8 +522,8 @@ int bp_fused_span_host(int arith, int pbytes, int fbytes, void* xs, void* ys, vo
     return BP_EINVAL;
   }
   if (count == 0) return BP_OK;
-  std::lock_guard<std::mutex> lock(g_host_mu);
-  HostCtx& h = g_host;
+  HostLease lease;
+  HostCtx& h = *lease.h;
   const int64_t nn = (geo_i[0] + 1) * (geo_i[1] + 1) * (geo_i[2] + 1);
   int64_t batch = batch_particles > 0 ? batch_particles : ((int64_t)1 << 21);
   if (batch > count) batch = count;

@@ -1,6 +1,7 @@
 // Internal interface between the C ABI (bp_capi.cu) and the kernel
 // translation units (bp_parity.cu: -fmad=false, bp_fast.cu: FMA).
 #pragma once
+#include <mutex>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -108,15 +109,23 @@ void timing_end(int handle, cudaStream_t s);
 // keep the default stream-ordered pool's memory mapped between calls
 void ensure_pool();
 
-// True the first time it is called for the current device with this flag
-// array (kernel attributes such as the dynamic shared memory limit are per
-// device, so a process driving two GPUs must set them on each).
-inline bool first_on_device(bool (&flags)[64]) {
+// Runs `set` once per device for this flag array (kernel attributes such as
+// the dynamic shared memory limit are per device, so a process driving two
+// GPUs must set them on each).  Thread-safe: a concurrent caller returns only
+// after `set` has run (the host pipeline is called from thread pools).
+template <class F>
+inline void once_per_device(bool (&flags)[64], F&& set) {
+  static std::mutex mu;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
-  if (flags[dev]) return false;
-  flags[dev] = true;
-  return true;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    set();
+    return;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (!flags[dev]) {
+    set();
+    flags[dev] = true;
+  }
 }
 
 }  // namespace bp

@@ -129,8 +129,9 @@ int launch_span(const SpanParams<typename Pol::P, typename Pol::F>& a, int64_t c
   // a push-only launch without TMA tiles touches no shared memory
   const size_t smem = a.bulk ? kFull : (DEP ? kStageOnly : 0);
   static bool attr[64] = {};
-  if (first_on_device(attr))
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFull);
+  });
   // one wave of resident blocks; every warp walks a contiguous run of >= 32
   const int grid = grid_for(k, smem, count, kThreads);
   const int th = timing_begin(TK_SPAN, s);

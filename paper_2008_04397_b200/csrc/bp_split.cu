@@ -610,8 +610,9 @@ int launch_deposit_cfg(const sk::Params<T>& a, cudaStream_t s) {
   const size_t smem =
       (size_t)(256 / 32) * (sk::stage_len<T>() + sk::Patch<PX>::kLen) * sizeof(T);
   static bool attr[64] = {};
-  if (first_on_device(attr))
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
   const int g = grid_of(k, smem, (long long)CHUNK * 8, a.count);
   const int th = timing_begin(TK_DEPOSIT, s);
   k<<<g, 256, smem, s>>>(a);
@@ -742,7 +743,7 @@ int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
   const int th = timing_begin(TK_RECORDS, s);
   const size_t osm = (size_t)8 * sk::kPackTI * 48 * (pbytes == 8 ? 8 : 4);
   static bool attr[64] = {};
-  if (first_on_device(attr)) {
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(sk::pack_cells<double, double>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 8);
     cudaFuncSetAttribute(sk::pack_cells<float, double>,
@@ -751,7 +752,7 @@ int split_pack_records(int pbytes, int fbytes, const void* E, const void* B,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
     cudaFuncSetAttribute(sk::pack_cells<float, float>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * sk::kPackTI * 48 * 4);
-  }
+  });
   if (pbytes == 8) {
     if (fbytes == 8)
       sk::pack_cells<double, double><<<blocks, 256, osm, s>>>((const double*)E, (const double*)B,
