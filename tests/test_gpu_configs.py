@@ -137,3 +137,37 @@ def test_c5_uniform_loader(gpu, oracle, label):
     for name, r, t in zip("xyzuvw", ref, d[:6]):
         assert np.array_equal(r, t.cpu().numpy()), name
     assert np.array_equal(acc_ref, dacc.cpu().numpy())
+
+
+@pytest.mark.parametrize("arith", ["parity", "fast"])
+def test_host_pipeline_concurrent_calls(gpu, arith):
+    """Four threads call fused_span on host (numpy) arrays at once — the
+    reference's phase-3 thread pool — each with its own particles and
+    accumulator: every result bitwise the one of the same call made alone
+    (each call borrows its own pipeline, csrc/bp_capi.cu)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+    from paper_2008_04397_b200 import kernels as K
+    geom, p, E, B, inv, tail = _species0((32, 16, 16), "single", 1e-3)
+    base = [a.cpu().numpy() for a in p.arrays()]
+    n = p.n
+    dev = torch.cuda.current_device()
+
+    def run(seed):
+        rng = np.random.default_rng(seed)
+        perm = rng.permutation(n)  # each task its own particle order
+        arrs = [a[perm].copy() for a in base]
+        acc = np.zeros((10,) + geom.node_shape, np.int64)
+        torch.cuda.set_device(dev)
+        st = K.fused_span(*arrs, 0, n, E, B, acc, inv, *tail, arith=arith,
+                          batch_particles=100_003)
+        return st, arrs, acc
+
+    alone = [run(s) for s in range(4)]
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        together = list(pool.map(run, range(4)))
+    for (s1, a1, c1), (s2, a2, c2) in zip(alone, together):
+        assert s1 == s2 == 0
+        for x, y in zip(a1, a2):
+            assert np.array_equal(x, y)
+        assert np.array_equal(c1, c2)
