@@ -122,15 +122,32 @@ struct KeyGeo {
 
 // ---------------------------------------------------------------------------
 // Migration: every listed leaver claims a slot at the end of its new bin.
+// A warp's 32 leavers come from one or two source bins, so they go to a few
+// neighbouring cells: lanes with the same destination are grouped
+// (__match_any_sync) and claim their slots with one atomic per group.
 template <typename S>
 __global__ void __launch_bounds__(256) migrate_bins(const __grid_constant__ BinsT<S> b) {
   const long long nl = min((long long)b.stat[ST_LEAVERS], b.lv_cap);
+  const unsigned lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
-    const LeaverT<S> L = b.lv[i];
-    const int dest = dest_of(L.b.w);
-    if (dest < 0 || dest >= b.ncell) continue;
-    const int pos = atomicAdd(&b.count[dest], 1);
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < nl;
+       i0 += stride) {
+    const long long i = i0 + lane;
+    LeaverT<S> L{};
+    int dest = -1;
+    if (i < nl) {
+      L = b.lv[i];
+      dest = dest_of(L.b.w);
+    }
+    const bool ok = dest >= 0 && dest < b.ncell;
+    const unsigned grp = __match_any_sync(0xffffffffu, ok ? dest : -1);
+    const int leader = __ffs(grp) - 1;
+    int pos = 0;
+    if (ok && (int)lane == leader) pos = atomicAdd(&b.count[dest], __popc(grp));
+    pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(grp & lt);
+    if (!ok) continue;
     const long long s = b.start[dest];
     if (pos < b.start[dest + 1] - s) {
       const long long d = s + pos;
