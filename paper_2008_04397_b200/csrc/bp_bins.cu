@@ -87,8 +87,12 @@ constexpr int kHoleCap = 256;    // leavers per bin per cycle tracked for the re
 constexpr int kMoveClaim = 8;    // bins per mover work claim (at most; Bins::move_claim)
 constexpr int kLvChunk = 128;    // leaver slots per warp reservation
 constexpr int kDepClaim = 16;    // bins per deposit work claim, 4 rounds of 4 (at most)
-constexpr int kRowS = 84;        // deposit transpose row stride (floats)
-constexpr int kWarpSm = 32 * kRowS + 32;
+// deposit flush rows: lane L's 80 sums corner-major (10 moments + 2 pad per
+// corner), rows 100 floats apart so the 8 lanes of a quarter write 4 banks
+// apart and a reader's corner is 3 contiguous float4
+constexpr int kCornerS = 12;
+constexpr int kRowS = 8 * kCornerS + 4;
+constexpr int kWarpSm = 32 * kRowS;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -636,9 +640,10 @@ __global__ void __launch_bounds__(256) deposit_list(const __grid_constant__ P a,
 // Lane l accumulates for its particles the 80 products q w_c m_k in
 // registers: A[k][cp] holds corners (2cp, 2cp + 1) of moment k, so one FFMA2
 // multiplies a corner pair of bases by a broadcast moment value.  The flush
-// writes each lane's 80 sums as a row of shared memory ([k][c], 20 x
+// writes each lane's 80 sums as a corner-major row of shared memory (24 x
 // STS.128), and lane (q, l) then adds corner l's 10 moments over its
-// quarter's 8 rows (quarter offset 8q: the 32 lanes read 32 distinct banks).
+// quarter's 8 rows (3 x LDS.128 and 5 FADD2 per row; against 80 scalar LDS
+// and 80 FADD in [moment][corner] rows: 0.509 -> 0.505 ms at C3).
 // The next particle of each lane (same bin, or the next round's bin) is
 // loaded while the current one is accumulated.
 // measured (scripts/build_variants.sh): 4 particles per lane in flight at
@@ -662,8 +667,8 @@ __device__ __forceinline__ void deposit_bins_body(const P& a, const Bins& b, flo
   const unsigned lane = threadIdx.x & 31;
   const int qd = (int)(lane >> 3), l = (int)(lane & 7);
   float* const ws = dsm + (threadIdx.x >> 5) * kWarpSm;
-  float* const myrow = ws + lane * kRowS + 8 * qd;
-  const float* const rd = ws + (8 * qd) * kRowS + 8 * qd + l;
+  float* const myrow = ws + lane * kRowS;
+  const float* const rd = ws + (8 * qd) * kRowS + l * kCornerS;
   const int ci_off = l & 1, cj_off = (l >> 1) & 1, ck_off = (l >> 2) & 1;
   constexpr int U = BP_DEP_UNR;
   float n1[U][7];
@@ -776,23 +781,35 @@ __device__ __forceinline__ void deposit_bins_body(const P& a, const Bins& b, flo
         }
       }
       if (nit > 0) {
-        // ---- flush: transpose through shared memory, then one corner per lane
+        // ---- flush: transpose through shared memory (corner-major rows),
+        // then lane (q, l) sums corner l's 10 moments over its quarter's rows
 #pragma unroll
-        for (int k = 0; k < 10; ++k) {
-          reinterpret_cast<float4*>(myrow + 8 * k)[0] =
-              make_float4(A[k][0].x, A[k][0].y, A[k][1].x, A[k][1].y);
-          reinterpret_cast<float4*>(myrow + 8 * k)[1] =
-              make_float4(A[k][2].x, A[k][2].y, A[k][3].x, A[k][3].y);
+        for (int c = 0; c < 8; ++c) {
+          float v[10];
+#pragma unroll
+          for (int k = 0; k < 10; ++k) v[k] = (c & 1) ? A[k][c >> 1].y : A[k][c >> 1].x;
+          float4* o = reinterpret_cast<float4*>(myrow + c * kCornerS);
+          o[0] = make_float4(v[0], v[1], v[2], v[3]);
+          o[1] = make_float4(v[4], v[5], v[6], v[7]);
+          o[2] = make_float4(v[8], v[9], 0.f, 0.f);
         }
         __syncwarp();
-        float sm[10];
+        F2 s2[5];
 #pragma unroll
-        for (int k = 0; k < 10; ++k) sm[k] = 0.f;
+        for (int k = 0; k < 5; ++k) s2[k] = f2(0.f, 0.f);
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int k = 0; k < 10; ++k) sm[k] += rd[r * kRowS + 8 * k];
+        for (int r = 0; r < 8; ++r) {
+          const float4* q = reinterpret_cast<const float4*>(rd + r * kRowS);
+          const float4 x0 = q[0], x1 = q[1], x2 = q[2];
+          s2[0] = __fadd2_rn(s2[0], f2(x0.x, x0.y));
+          s2[1] = __fadd2_rn(s2[1], f2(x0.z, x0.w));
+          s2[2] = __fadd2_rn(s2[2], f2(x1.x, x1.y));
+          s2[3] = __fadd2_rn(s2[3], f2(x1.z, x1.w));
+          s2[4] = __fadd2_rn(s2[4], f2(x2.x, x2.y));
+        }
         __syncwarp();
+        const float sm[10] = {s2[0].x, s2[0].y, s2[1].x, s2[1].y, s2[2].x,
+                              s2[2].y, s2[3].x, s2[3].y, s2[4].x, s2[4].y};
         if (okb && n > 0) {
           const int node = ((q3.i + ci_off) * a.NY + (q3.j + cj_off)) * a.NZ + q3.k + ck_off;
           const double iv =
