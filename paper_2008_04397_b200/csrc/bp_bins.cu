@@ -303,7 +303,14 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 #ifndef BP_MOVER_MINB
 #define BP_MOVER_MINB 5   // resident blocks per SM it is compiled for (<= 102 registers)
 #endif
+#ifndef BP_MOVER_IDPF
+#define BP_MOVER_IDPF 1   // L2 prefetch of each bin's ids at the bin's start
+#endif
 constexpr int kMoverWarps = BP_MOVER_TPB / 32;
+
+__device__ __forceinline__ void prefetch_l2(uintptr_t p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 template <bool RX, bool RY, bool RZ, int NIT>
 __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const __grid_constant__ P a,
@@ -442,6 +449,16 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
       }
       if (n > 0) {
         if (!pf_ok) fetch(s0 + lane, (int)lane < n);
+#if BP_MOVER_IDPF
+        {
+          // the bin's ids are read only by the refill at the bin's end (the
+          // leavers' ids and the trailing stayers'): bring their lines from
+          // DRAM into L2 now, one 128-byte line per lane (bins up to 512)
+          const uintptr_t i0 = reinterpret_cast<uintptr_t>(b.id + s0);
+          const uintptr_t ln = (i0 & ~(uintptr_t)127) + ((uintptr_t)lane << 7);
+          if (ln <= reinterpret_cast<uintptr_t>(b.id + s0 + n - 1)) prefetch_l2(ln);
+        }
+#endif
 #if BP_MOVER_WINDOW
         const float4* rs = win_s[wid] + (1 + c - c0) * 12;
 #else
