@@ -166,6 +166,10 @@ class DeviceSimulation:
         # precision (bp_field_records_build), built once per field update and
         # shared by every species' call (f32, mixed, and f64 with f64 fields)
         self.records = None
+        # run_cycle(stream_moments=True): the copy stream still writing the
+        # pinned moment buffers, and whether the last cycle streamed them
+        self._moments_copy_pending = None
+        self._moments_streamed = False
         self._records_fresh = False
         self._records_pbytes = 4 if pd == torch.float32 else 8
         if self.arith == "fast":
@@ -331,12 +335,23 @@ class DeviceSimulation:
             ss.wait_stream(s)
         return self._side
 
-    def phase3(self, reduce=True):
+    def phase3(self, reduce=True, stream_moments=False):
         """Phases 2-3 for every species; returns (phase3_ms, kernel_ms) of
-        device time on the compute stream (events), reduce included."""
+        device time on the compute stream (events), reduce included.
+
+        ``stream_moments`` (single rank): each species' grid is folded right
+        after its kernels and copied to its pinned host buffer on a copy
+        stream while the next species runs (moments_host(reuse=True) then
+        only waits for the last copy)."""
         torch = self.torch
         s = torch.cuda.current_stream(self.device)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        stream_moments = stream_moments and not self.distributed
+        cs = self._copy_stream() if stream_moments else None
+        if self._moments_copy_pending is not None:
+            # the previous cycle's host copies read the grids zeroed below
+            s.wait_stream(self._moments_copy_pending)
+        self._moments_copy_pending = None
         self.status.zero_()
         ev[0].record(s)
         for a in self.acc:
@@ -367,6 +382,12 @@ class DeviceSimulation:
                     s.wait_stream(ss)
                 works += reduce_moments([self.acc[sid]], self.group, async_op=True,
                                         root=0 if self.reduce == "root" else None)
+            if cs is not None:
+                self._fold_one(self.acc[sid], ss)
+                cs.wait_stream(ss)
+                h = self._pinned(f"_mom_host_{sid}", self.acc[sid])
+                with torch.cuda.stream(cs):
+                    h.copy_(self.acc[sid], non_blocking=True)
         for ss in side:
             s.wait_stream(ss)
         ev[2].record(s)
@@ -378,6 +399,15 @@ class DeviceSimulation:
             # others in the next collective)
             import torch.distributed as dist
             dist.all_reduce(self.status, op=dist.ReduceOp.MAX, group=self.group)
+        if cs is not None:
+            # species without particles: zero grids, nothing to fold
+            for sid, n in enumerate(self._species_n()):
+                if n == 0:
+                    h = self._pinned(f"_mom_host_{sid}", self.acc[sid])
+                    cs.wait_stream(s)
+                    with torch.cuda.stream(cs):
+                        h.copy_(self.acc[sid], non_blocking=True)
+            self._moments_copy_pending = cs
         ev[3].synchronize()
         st = int(self.status.item())
         if self.binned:
@@ -408,14 +438,24 @@ class DeviceSimulation:
 
     def fold_moments(self):
         """Phase 4 on device: merge duplicated periodic planes (exact)."""
-        L = _lib.load()
-        gi = np.ascontiguousarray(self.geo_i, np.int64)
         s = self.torch.cuda.current_stream(self.device)
         for a in self.acc:
-            rc = L.bp_fold_periodic_i64(ctypes.c_void_p(a.data_ptr()), N_MOMENTS,
-                                        ctypes.c_void_p(gi.ctypes.data),
-                                        ctypes.c_void_p(s.cuda_stream))
-            _lib.check(rc, "fold_periodic")
+            self._fold_one(a, s)
+
+    def _fold_one(self, a, stream):
+        L = _lib.load()
+        gi = np.ascontiguousarray(self.geo_i, np.int64)
+        rc = L.bp_fold_periodic_i64(ctypes.c_void_p(a.data_ptr()), N_MOMENTS,
+                                    ctypes.c_void_p(gi.ctypes.data),
+                                    ctypes.c_void_p(stream.cuda_stream))
+        _lib.check(rc, "fold_periodic")
+
+    def _copy_stream(self):
+        cs = getattr(self, "_mom_copy_stream", None)
+        if cs is None:
+            cs = self.torch.cuda.Stream(device=self.device)
+            self._mom_copy_stream = cs
+        return cs
 
     def _pinned(self, attr, like):
         """Persistent pinned host tensor shaped like ``like`` (lazily made)."""
@@ -431,6 +471,11 @@ class DeviceSimulation:
         by the next call) instead of fresh arrays."""
         if not reuse:
             return [a.cpu().numpy() for a in self.acc]
+        if self._moments_streamed:
+            # run_cycle(stream_moments=True) already queued the copies
+            self._moments_copy_pending.synchronize()
+            return [self._pinned(f"_mom_host_{sid}", a).numpy()
+                    for sid, a in enumerate(self.acc)]
         out = []
         for sid, a in enumerate(self.acc):
             h = self._pinned(f"_mom_host_{sid}", a)
@@ -477,9 +522,13 @@ class DeviceSimulation:
             if p is not None:
                 p.sort_by_cell(self.geom)
 
-    def run_cycle(self, E=None, B=None):
+    def run_cycle(self, E=None, B=None, stream_moments=False):
         """One cycle on device: phases 1-4 and (when due) 6.  The host solve
         (phase 5) is the caller's; moments for it are in ``self.acc``.
+
+        ``stream_moments=True`` (single rank): each species' folded grid is
+        copied to pinned host memory while the next species runs;
+        ``moments_host(reuse=True)`` returns those buffers.
 
         Distributed: every rank calls this collectively; rank 0 passes the new
         E/B (others may pass None) and the broadcast runs on all ranks."""
@@ -489,8 +538,12 @@ class DeviceSimulation:
         # phase 1 always refreshes the cell records (a cycle's fields are new
         # in a real run, even when the caller updated self.E / self.B in place)
         self._records_fresh = False
-        p3, kt = self.phase3()
-        self.fold_moments()
+        streamed = stream_moments and not self.distributed
+        self._moments_streamed = False
+        p3, kt = self.phase3(stream_moments=streamed)
+        self._moments_streamed = streamed
+        if not streamed:
+            self.fold_moments()
         sort_ms, sorted_now = 0.0, False
         if (not self.binned and self.sort_period > 0
                 and (self.cycle + 1) % self.sort_period == 0):

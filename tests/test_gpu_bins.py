@@ -318,3 +318,33 @@ def test_bins_two_streams_match_one(gpu, label, monkeypatch):
         da, db = _by_id(pa), _by_id(pb)
         for k in da:
             assert np.array_equal(da[k], db[k]), k
+
+
+@pytest.mark.parametrize("layout,label", [("bins", "single"), ("flat", "single"),
+                                          ("bins", "double")])
+def test_streamed_moments_equal_the_cycle_end_copy(gpu, layout, label, monkeypatch):
+    """run_cycle(stream_moments=True) folds each species' grid right after its
+    kernels and copies it to pinned host memory while the next species runs.
+    The host copies must be the final device grids bitwise (no copy may race
+    the fold or a later kernel), cycle after cycle, also with the species on
+    two streams and with overflowing bins (zero headroom); and they must
+    match the default path (fold after the cycle, one copy per species):
+    bitwise where the arithmetic is order-independent (flat f32, f64 bins),
+    within the f32 tolerance on the f32 bins, whose per-bin sums follow the
+    migration's atomic order."""
+    geom, species, prec, bufs, fields = _gem(label=label)
+    for streams in ("0", "2"):
+        monkeypatch.setenv("BP_BIN_STREAMS", streams)
+        monkeypatch.setenv("BP_SPECIES_STREAMS", streams)
+        kw = {"bin_slack": (0.0, 0)} if layout == "bins" else {}
+        a = _sim(geom, species, prec, bufs, layout, **kw)
+        b = _sim(geom, species, prec, bufs, layout, **kw)
+        for cyc in range(4):
+            a.run_cycle(fields.E, fields.B)
+            b.run_cycle(fields.E, fields.B, stream_moments=True)
+            ma = [m.copy() for m in a.moments_host(reuse=True)]
+            mb = [m.copy() for m in b.moments_host(reuse=True)]
+            for x, y in zip(mb, b.acc):
+                assert np.array_equal(x, y.cpu().numpy()), (streams, cyc)
+            exact = layout == "flat" or label == "double"
+            _assert_moments_close(ma, mb, 0 if exact else _tol(label))
