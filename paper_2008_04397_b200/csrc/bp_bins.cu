@@ -42,6 +42,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "bp_f32_common.cuh"
 #include "bp_bins_plumb.cuh"
@@ -190,8 +191,15 @@ __device__ __forceinline__ int win_slot(const Win& W, int i, int j, int k) {
 
 // NIT > 0: the iteration count as a compile-time constant (fully unrolled);
 // NIT == 0: a.n_iters at run time
-template <bool RX, bool RY, bool RZ, int NIT>
-__device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, int home,
+// FC (grids below 2^24 cells): the midpoint's cell index and fractions in
+// float — trunc, clamp and the x-fastest index are exact there, fx = gx - i
+// bitwise as cell_of — so the per-iteration reload test needs no F2I / I2F
+// round trip; `held` / `home` are then float cell indices.
+template <bool FC>
+using HeldT = typename std::conditional<FC, float, int>::type;
+
+template <bool RX, bool RY, bool RZ, int NIT, bool FC>
+__device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], HeldT<FC>& held, HeldT<FC> home,
                                         const float4* home_rec, const Win& W, float& xp,
                                         float& yp, float& zp, float& un, float& vn, float& wn,
                                         bool skipbc) {
@@ -214,8 +222,20 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
       }
     }
     float fx, fy, fz;
-    int i, j, k;
-    const int cell = sk::cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    int i = 0, j = 0, k = 0;
+    HeldT<FC> cell;
+    if constexpr (FC) {
+      const F2 G = fma2(f2(xm, ym), f2(a.idx[0], a.idx[1]), f2(-a.ogs[0], -a.ogs[1]));
+      const float gz = fmaf(zm, a.idx[2], -a.ogs[2]);
+      const float tx = fminf(truncf(G.x), a.nm1[0]), ty = fminf(truncf(G.y), a.nm1[1]);
+      const float tz = fminf(truncf(gz), a.nm1[2]);
+      fx = G.x - tx;
+      fy = G.y - ty;
+      fz = gz - tz;
+      cell = fmaf(tz, a.cnyf, fmaf(ty, a.nxf, tx));
+    } else {
+      cell = sk::cell_of(a, xm, ym, zm, fx, fy, fz, i, j, k);
+    }
     float ex, ey, hx, hy, ez, hz;
     const bool need = cell != held;
     if (__any_sync(0xffffffffu, need)) {
@@ -234,7 +254,7 @@ __device__ __forceinline__ int push_bin(const P& a, float4 (&R)[12], int& held, 
             load_record(a, cell, R);
           }
 #else
-          load_record(a, cell, R);
+          load_record(a, (int)cell, R);
 #endif
         }
       }
@@ -303,6 +323,12 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 #ifndef BP_MOVER_MINB
 #define BP_MOVER_MINB 5   // resident blocks per SM it is compiled for (<= 102 registers)
 #endif
+#ifndef BP_MOVER_FCELL
+#define BP_MOVER_FCELL 1  // float midpoint cell index where exact (< 2^24 cells)
+#endif
+#if BP_MOVER_WINDOW && BP_MOVER_FCELL
+#error "the field window needs the integer cell coordinates (build with -DBP_MOVER_FCELL=0)"
+#endif
 #ifndef BP_MOVER_IDPF
 #define BP_MOVER_IDPF 1   // L2 prefetch of each bin's ids at the bin's start
 #endif
@@ -312,7 +338,7 @@ __device__ __forceinline__ void prefetch_l2(uintptr_t p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <bool RX, bool RY, bool RZ, int NIT>
+template <bool RX, bool RY, bool RZ, int NIT, bool FC>
 __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const __grid_constant__ P a,
                                                      const __grid_constant__ Bins b) {
 #if BP_MOVER_WINDOW
@@ -467,7 +493,8 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 #pragma unroll
         for (int q = 0; q < 12; ++q) R[q] = rs[q];
         const float vmax = bin_speed_bound(a, q3, qe, hmin, epsmax);
-        int held = c;
+        HeldT<FC> held = (HeldT<FC>)c;
+        const HeldT<FC> homec = (HeldT<FC>)c;
         int nh = 0;
 #pragma unroll 1
         for (int t0 = 0; t0 < n; t0 += 32) {
@@ -491,7 +518,8 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           const bool all_in =
               __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
           const int st =
-              push_bin<RX, RY, RZ, NIT>(a, R, held, c, rs, W, xp, yp, zp, un, vn, wn, all_in);
+              push_bin<RX, RY, RZ, NIT, FC>(a, R, held, homec, rs, W, xp, yp, zp, un, vn, wn,
+                                            all_in);
           int dest = c;
           if (st == ST_OK) {
             // the new cell (cell_of's formula, bp_f32_common.cuh)
@@ -892,7 +920,15 @@ int resident_grid(K k, size_t smem, int threads = 256) {
 template <bool RX, bool RY, bool RZ>
 int launch_mover_bins(const bins::P& a, const bins::Bins& b, cudaStream_t s) {
   // the reference's default of 3 midpoint iterations unrolled
-  auto k = a.n_iters == 3 ? bins::mover_bins<RX, RY, RZ, 3> : bins::mover_bins<RX, RY, RZ, 0>;
+#if BP_MOVER_FCELL
+  // float cell indices are exact below 2^24 cells
+  auto k = a.n_iters != 3                  ? bins::mover_bins<RX, RY, RZ, 0, false>
+           : (long long)a.cny * a.nz < (1 << 24) ? bins::mover_bins<RX, RY, RZ, 3, true>
+                                                 : bins::mover_bins<RX, RY, RZ, 3, false>;
+#else
+  auto k = a.n_iters == 3 ? bins::mover_bins<RX, RY, RZ, 3, false>
+                          : bins::mover_bins<RX, RY, RZ, 0, false>;
+#endif
   const int g = resident_grid(k, 0, BP_MOVER_TPB);
   // claims of up to 8 bins, fewer on small grids so that every warp gets
   // several claims (the dynamic claiming then balances the tail)

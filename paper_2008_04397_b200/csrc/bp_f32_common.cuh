@@ -31,6 +31,8 @@ struct Params {
   unsigned* skip;            // one bit per span particle the mover did not store
   const float* emax;         // max |E| over the nodes (after the cell records)
   T bc_eps[3];               // rounding slack of the boundary-skip test per axis
+  T nm1[3];                  // cell counts - 1, and nx, nx * ny, in T (float cell index)
+  T nxf, cnyf;
 };
 
 // record quad of T

@@ -673,6 +673,8 @@ void fill_params(const Call& c, sk::Params<T>& a) {
   a.nx = (int)c.geo_i[0]; a.ny = (int)c.geo_i[1]; a.nz = (int)c.geo_i[2];
   a.NY = a.ny + 1; a.NZ = a.nz + 1; a.NN = (a.nx + 1) * a.NY * a.NZ;
   a.cny = a.nx * a.ny;
+  a.nm1[0] = (T)(a.nx - 1); a.nm1[1] = (T)(a.ny - 1); a.nm1[2] = (T)(a.nz - 1);
+  a.nxf = (T)a.nx; a.cnyf = (T)a.cny;
   for (int k = 0; k < 3; ++k) {
     const T o = (T)c.geo_f[3 + k], L = (T)c.geo_f[6 + k];
     const T hi = o + L;  // particle-precision sum, as the reference
