@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
     return (int)min(__shfl_sync(0xffffffffu, c, 0), (unsigned long long)b.ncell);
   };
 #endif
+  int st_worst = ST_OK;  // the lane's worst push status (ST_OK = 0 < errors)
   // the warp's current chunk of leaver slots [lv_base, lv_base + kLvChunk),
   // lv_used of them taken (starts "full": the first leaver claims a chunk)
   int lv_base = 0, lv_next = 0;
@@ -530,7 +531,9 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
                       k = min((int)gz, a.nz - 1);
             dest = i + a.nx * j + a.cny * k;
           } else if (valid) {
-            atomicMax(a.status, st);  // not stored (kernels.py:618-621); the cycle raises
+            // not stored (kernels.py:618-621); the cycle raises.  Reported
+            // once per lane at the end: no atomic path in the tile loop
+            st_worst = max(st_worst, st);
           }
         const bool leave = valid && st == ST_OK && dest != c;
         const unsigned L = __ballot_sync(0xffffffffu, leave);
@@ -642,6 +645,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   // unused slots of the last leaver chunk carry no particle
   for (int k = lv_used + (int)lane; k < kLvChunk; k += 32)
     if (lv_base + k < b.lv_cap) b.lv[lv_base + k].b.w = __int_as_float(-1);
+  if (st_worst != ST_OK) atomicMax(a.status, st_worst);
 }
 
 // ---------------------------------------------------------------------------

@@ -348,3 +348,19 @@ def test_streamed_moments_equal_the_cycle_end_copy(gpu, layout, label, monkeypat
                 assert np.array_equal(x, y.cpu().numpy()), (streams, cyc)
             exact = layout == "flat" or label == "double"
             _assert_moments_close(ma, mb, 0 if exact else _tol(label))
+
+
+@pytest.mark.parametrize("label", ["single", "double"])
+def test_bins_report_failing_particles(gpu, label):
+    """A particle that would leave the box (kernels.py:618-621) is not stored
+    and the cycle raises, on the bins as on the flat layout (the binned mover
+    reports each lane's worst status once, at the end of the kernel)."""
+    from paper_2008_04397_b200.errors import IntegrityError
+    geom, species, prec, bufs, fields = _gem(label=label)
+    for layout in ("bins", "flat"):
+        bad = [b.copy() for b in bufs]
+        bad[0].u[7] = bad[0].u.dtype.type(1e3)  # 250 box lengths in one step
+        sim = _sim(geom, species, prec, bad, layout)
+        assert sim.binned == (layout == "bins")
+        with pytest.raises(IntegrityError):
+            sim.run_cycle(fields.E, fields.B)
