@@ -443,12 +443,11 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 #endif
   // prefetched particle (one per lane) and the slot it came from
   float4 n1a = make_float4(0.f, 0.f, 0.f, 0.f), n1b = n1a;
-  auto fetch = [&](int q, bool ok) {
-    if (ok) {
-      // streaming loads (read once per cycle): the 32-byte record
-      ld_rec_stream(slot_rec(b.rec, q), n1a, n1b);
-    }
-  };
+  // streaming loads (read once per cycle): the 32-byte record of slot q, or
+  // (lanes past the end of the tile's bin) of the tile's first slot q0 — a
+  // broadcast in lane 0's sector — so those lanes push a copy of lane 0's
+  // particle (not stored) and the whole warp runs the push
+  auto fetch = [&](int q, bool ok, int q0) { ld_rec_stream(slot_rec(b.rec, ok ? q : q0), n1a, n1b); };
   float4 R[12];
   while (c0 < b.ncell) {
     const int c1 = min(c0 + b.move_claim, b.ncell);
@@ -462,7 +461,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
 #endif
     int s0 = (int)b.start[c0];
     int n = min(b.count[c0], (int)b.start[c0 + 1] - s0);
-    fetch(s0 + lane, (int)lane < n);
+    if (n > 0) fetch(s0 + lane, (int)lane < n, s0);
     bool pf_ok = true;  // (warp-uniform) n1 holds this bin's first tile
     Ijk q3 = ijk_of(a, c0);
     for (int c = c0; c < c1; ++c, q3 = ijk_advance(a, q3, 1)) {
@@ -475,7 +474,7 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
         n_1 = min(b.count[c + 1], (int)b.start[c + 2] - s1);
       }
       if (n > 0) {
-        if (!pf_ok) fetch(s0 + lane, (int)lane < n);
+        if (!pf_ok) fetch(s0 + lane, (int)lane < n, s0);
 #if BP_MOVER_IDPF
         {
           // the bin's ids are read only by the refill at the bin's end (the
@@ -504,18 +503,8 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           const int p = s0 + r;
           float xp = n1a.x, yp = n1a.y, zp = n1a.z, un = n1a.w, vn = n1b.x, wn = n1b.y;
           const float qp = n1b.z;
-          if (t0 + 32 < n) fetch(p + 32, r + 32 < n);
-          else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1);
-          if (n - t0 < 32) {
-            // the lanes past the bin's end push a copy of lane 0's particle
-            // (not stored), so the whole warp runs the push
-            const float c0x = __shfl_sync(0xffffffffu, xp, 0), c0y = __shfl_sync(0xffffffffu, yp, 0);
-            const float c0z = __shfl_sync(0xffffffffu, zp, 0), c0u = __shfl_sync(0xffffffffu, un, 0);
-            const float c0v = __shfl_sync(0xffffffffu, vn, 0), c0w = __shfl_sync(0xffffffffu, wn, 0);
-            if (!valid) {
-              xp = c0x; yp = c0y; zp = c0z; un = c0u; vn = c0v; wn = c0w;
-            }
-          }
+          if (t0 + 32 < n) fetch(p + 32, r + 32 < n, s0 + t0 + 32);
+          else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1, s1);
           const bool all_in =
               __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
           const int st =
