@@ -144,6 +144,16 @@ __device__ __forceinline__ bool in_box(const Box& b, float gx, float gy, float g
          gz < b.hi[2];
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ void load_record(const P& a, int cell, float4 (&R)[12]) {
   const float4* r = static_cast<const float4*>(a.rec) + (size_t)cell * 12;
 #pragma unroll
@@ -323,6 +333,9 @@ __device__ __forceinline__ float bin_speed_bound(const P& a, Ijk q, float qe, fl
 #ifndef BP_MOVER_MINB
 #define BP_MOVER_MINB 5   // resident blocks per SM it is compiled for (<= 102 registers)
 #endif
+#ifndef BP_MOVER_SMP
+#define BP_MOVER_SMP 1    // next particle staged in shared memory by cp.async (0: registers)
+#endif
 #ifndef BP_MOVER_FCELL
 #define BP_MOVER_FCELL 1  // float midpoint cell index where exact (< 2^24 cells)
 #endif
@@ -349,6 +362,9 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   __shared__ __align__(8) unsigned long long bars_s[kMoverWarps][2];
   // hole slots within the bin (< 65536) and the leavers' list slots (< 2^31:
   // the list holds a quarter of the species + 1M)
+#if BP_MOVER_SMP
+  __shared__ __align__(16) float4 pst_s[kMoverWarps][64];  // next particle of each lane
+#endif
   __shared__ unsigned short holes_s[kMoverWarps][kHoleCap];
   __shared__ int lvslot_s[kMoverWarps][kHoleCap];
   const int wid = threadIdx.x >> 5;
@@ -447,7 +463,18 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
   // (lanes past the end of the tile's bin) of the tile's first slot q0 — a
   // broadcast in lane 0's sector — so those lanes push a copy of lane 0's
   // particle (not stored) and the whole warp runs the push
+#if BP_MOVER_SMP
+  // the next particle goes global -> shared (cp.async, no registers held
+  // across the push), read back at the next tile's top
+  float4* const pmine = pst_s[wid] + 2 * lane;
+  auto fetch = [&](int q, bool ok, int q0) {
+    const float4* g = slot_rec(b.rec, ok ? q : q0);
+    cp_async16(pmine, g);
+    cp_async16(pmine + 1, g + 1);
+  };
+#else
   auto fetch = [&](int q, bool ok, int q0) { ld_rec_stream(slot_rec(b.rec, ok ? q : q0), n1a, n1b); };
+#endif
   float4 R[12];
   while (c0 < b.ncell) {
     const int c1 = min(c0 + b.move_claim, b.ncell);
@@ -501,12 +528,25 @@ __global__ void __launch_bounds__(BP_MOVER_TPB, BP_MOVER_MINB) mover_bins(const 
           const int r = t0 + (int)lane;
           const bool valid = r < n;
           const int p = s0 + r;
+#if BP_MOVER_SMP
+          cp_async_wait_all();
+          n1a = pmine[0];
+          n1b = pmine[1];
+#endif
           float xp = n1a.x, yp = n1a.y, zp = n1a.z, un = n1a.w, vn = n1b.x, wn = n1b.y;
           const float qp = n1b.z;
+#if !BP_MOVER_SMP
           if (t0 + 32 < n) fetch(p + 32, r + 32 < n, s0 + t0 + 32);
           else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1, s1);
+#endif
           const bool all_in =
               __all_sync(0xffffffffu, fabsf(un) + fabsf(vn) + fabsf(wn) < vmax);
+#if BP_MOVER_SMP
+          // the lane's slot is refilled only after the vote has consumed its
+          // particle (both shared loads have returned)
+          if (t0 + 32 < n) fetch(p + 32, r + 32 < n, s0 + t0 + 32);
+          else if (n_1 > 0) fetch(s1 + lane, (int)lane < n_1, s1);
+#endif
           const int st =
               push_bin<RX, RY, RZ, NIT, FC>(a, R, held, homec, rs, W, xp, yp, zp, un, vn, wn,
                                             all_in);
