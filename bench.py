@@ -117,8 +117,8 @@ def peaks():
 
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the newest committed ncu capture
-    summary that has it (profiles/ncu_summary_r02o.json, then r02n, r02m, r02h, r02f, r02e, r02b), or None."""
-    for tag in ("r02o", "r02n", "r02m", "r02h", "r02f", "r02e", "r02b"):
+    summary that has it (profiles/ncu_summary_r02p.json, then r02o, r02n, r02m, r02h, r02f, r02e, r02b), or None."""
+    for tag in ("r02p", "r02o", "r02n", "r02m", "r02h", "r02f", "r02e", "r02b"):
         try:
             with open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.json")) as f:
                 return float(json.load(f)[kernel]["dram_bytes_per_launch"])
